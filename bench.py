@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""Benchmark of the FSS hot path on B200 (contract: see DESIGN.md "Measurement").
+
+Metric (BASELINE.json): FSS comparisons/sec, DCF eval, n = 32. One comparison =
+the evaluation of one element's DCF key by BOTH parties (two party-evals).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Default workload (`config.workload`): 2^24 DCF keys per GPU (n = out_bits = 32),
+keys resident in HBM in the reference's SoA layout (≈18 GB per GPU, far larger
+than the 126 MB L2, so no L2 flush is needed between steps). A step = eval_cmp
+for party 0 and party 1 over every element (two kernel launches).
+
+`e2e` = the same metric through the public drop-in API with host buffers: per
+step keygen_cmp(32, rng, N) from the host numpy Generator (tape drawn on device
+from its PCG64 state), eval_cmp for both parties on a pinned host x, shares
+copied back to pinned host memory. It includes keygen, so it is strictly more
+work per comparison than `value`.
+
+`--impl reference` times the CPU restatement of the reference's algorithm
+(oracle/, C + AES-NI + OpenMP on all host cores; the Python reference itself
+cannot travel to the GPU box) on a bounded sample of the same workload.
+Multi-GPU (torchrun): every rank holds its own slice of keys for both parties
+(weak scaling, no data-path collective); time = max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_BITS = 32
+BYTES_PER_EVAL = 16 + 32 * 16 + 32 + 32 * 8 + 33 * 8 + 8 + 8   # 1096 B
+AES_PER_EVAL = 64                                              # 32 levels x 2 blocks
+LDS_PER_AES = 160                                              # T-table lookups per block
+LDS_PER_CLK_SM = 32                                            # 128 B/clk smem crossbar
+
+
+def _args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--log2n", type=int, default=24, help="DCF keys per GPU = 2^log2n")
+    p.add_argument("--cpu-log2n", type=int, default=20, help="CPU sample size (reference arm)")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    return p.parse_args()
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# --------------------------------------------------------------- reference
+
+def run_reference(args, ws, rank):
+    """CPU arm: the oracle restatement of the reference algorithm on host cores."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+    oracle.build()
+    N = 1 << args.cpu_log2n
+    rng = np.random.default_rng(1)
+    alpha, k0, k1 = oracle.keygen_cmp(N_BITS, rng, N)
+    x = (alpha + np.random.default_rng(2).integers(0, 2000, N, dtype=np.uint64)
+         - np.uint64(1000)) & np.uint64(0xFFFFFFFF)
+    for _ in range(args.warmup):
+        oracle.eval_cmp(0, k0, x)
+        oracle.eval_cmp(1, k1, x)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        y0 = oracle.eval_cmp(0, k0, x)
+        y1 = oracle.eval_cmp(1, k1, x)
+        times.append(time.perf_counter() - t0)
+    rec = (y0 + y1) & np.uint64(0xFFFFFFFF)
+    assert np.array_equal(rec, (x <= alpha).astype(np.uint64))
+    t = sum(times) / len(times)
+    v = N / t
+    cores = oracle.threads()
+    line = {
+        "impl": "reference", "metric": "FSS comparisons/sec (DCF eval, n=32)", "value": v,
+        "unit": "comparisons/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"DCF eval n=32, both parties, bounded CPU sample of 2^{args.cpu_log2n} "
+                               f"keys (the GPU arm runs 2^{args.log2n} per GPU)",
+                   "global_batch": N, "parallelism": f"{cores} host threads"},
+        "cpu_baseline": {"value": v, "unit": "comparisons/s", "cores": cores, "kind": "port",
+                         "sample": f"2^{args.cpu_log2n} DCF keys, eval_cmp party 0 + party 1, "
+                                   f"oracle/fss_oracle.c (AES-NI={oracle.aesni()})"},
+        "e2e": {"value": v, "unit": "comparisons/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- ours
+
+def cpu_baseline_line(log2n: int):
+    import numpy as np
+
+    import oracle
+    oracle.build()
+    N = 1 << log2n
+    rng = np.random.default_rng(1)
+    alpha, k0, k1 = oracle.keygen_cmp(N_BITS, rng, N)
+    x = alpha.copy()
+    oracle.eval_cmp(0, k0, x)
+    reps, t_total = 0, 0.0
+    while t_total < 5.0 and reps < 20:
+        t0 = time.perf_counter()
+        oracle.eval_cmp(0, k0, x)
+        oracle.eval_cmp(1, k1, x)
+        t_total += time.perf_counter() - t0
+        reps += 1
+    return {"value": N * reps / t_total, "unit": "comparisons/s", "cores": oracle.threads(),
+            "kind": "port",
+            "sample": f"{reps} x 2^{log2n} DCF keys (n=32), eval_cmp party 0 + party 1, oracle C "
+                      f"restatement with AES-NI={oracle.aesni()}, OpenMP"}
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_dcf_eval.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get("dram_bytes_per_party_eval")
+    except (OSError, ValueError):
+        return None
+
+
+def run_ours(args, ws, rank, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2006_04593_b200 import _lib, fss
+
+    _lib.load()  # fail loudly without the CUDA library
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    N = 1 << args.log2n
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if ws == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- value: keys resident in HBM, device inputs ------------------------
+    rng = np.random.default_rng(1000 + rank)
+    alpha, k0, k1 = fss.keygen_cmp(N_BITS, rng, N, device=dev)
+    y = torch.randint(-(1 << 20), 1 << 20, (N,), device=dev, dtype=torch.int64)
+    x = ((alpha.view(torch.int64) + y) & 0xFFFFFFFF).view(torch.uint64)
+    out0 = out1 = None
+    for _ in range(args.warmup):
+        out0 = fss.eval_cmp(0, k0, x)
+        out1 = fss.eval_cmp(1, k1, x)
+    torch.cuda.synchronize()
+    rec = (out0.view(torch.int64) + out1.view(torch.int64)) & 0xFFFFFFFF
+    assert torch.equal(rec, (x.view(torch.int64) <= alpha.view(torch.int64)).to(torch.int64)), \
+        "DCF reconstruction mismatch"
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    stream = torch.cuda.current_stream(dev)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps + 1)]
+    barrier()
+    torch.cuda.synchronize()
+    evs[0].record(stream)
+    for s in range(args.steps):
+        fss.eval_cmp(0, k0, x)
+        evs[2 * s + 1].record(stream)
+        fss.eval_cmp(1, k1, x)
+        evs[2 * s + 2].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    launch_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(2 * args.steps)]
+    t_local = evs[0].elapsed_time(evs[-1]) / 1e3
+    t = max_over_ranks(t_local)
+    value = ws * N * args.steps / t
+    avg_launch_s = sum(launch_ms) / len(launch_ms) / 1e3
+
+    achieved_gbs = N * BYTES_PER_EVAL / avg_launch_s / 1e9
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except (OSError, ValueError):
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    traffic = load_traffic()
+    props = torch.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
+    aes_rate = N * AES_PER_EVAL / avg_launch_s
+    aes_peak = sms * sm_max * 1e6 * LDS_PER_CLK_SM / LDS_PER_AES
+    del out0, out1, rec
+
+    # ---- e2e through the public API with host buffers ----------------------
+    e2e = None
+    if not args.no_e2e:
+        del k0, k1, alpha, x, y
+        torch.cuda.empty_cache()
+        x_host = torch.empty(N, dtype=torch.int64, pin_memory=True)
+        x_host.copy_(torch.from_numpy(np.random.default_rng(5 + rank).integers(
+            0, 1 << 32, N, dtype=np.uint64).view(np.int64)))
+        x_host = x_host.view(torch.uint64)
+        rng2 = np.random.default_rng(2000 + rank)
+
+        def e2e_step():
+            a, q0, q1 = fss.keygen_cmp(N_BITS, rng2, N, device=dev)
+            r0 = fss.eval_cmp(0, q0, x_host)      # pinned host in -> pinned host out
+            r1 = fss.eval_cmp(1, q1, x_host)
+            return r0, r1
+
+        for _ in range(args.warmup):
+            r0, r1 = e2e_step()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e_start = torch.cuda.Event(enable_timing=True)
+        e_end = torch.cuda.Event(enable_timing=True)
+        e_start.record(stream)
+        for _ in range(args.steps):
+            r0, r1 = e2e_step()
+        e_end.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        t_e2e = max_over_ranks(max(e_start.elapsed_time(e_end) / 1e3, wall))
+        e2e = {"value": ws * N * args.steps / t_e2e, "unit": "comparisons/s",
+               "h2d_bytes_per_step": 2 * N * 8 + 48,
+               "d2h_bytes_per_step": 2 * N * 8,
+               "step": "keygen_cmp(32, numpy Generator, 2^%d) + eval_cmp(party 0/1, pinned host x) "
+                       "-> pinned host shares" % args.log2n}
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None if (args.no_cpu or ws > 1) else cpu_baseline_line(16)
+    line = {
+        "metric": "FSS comparisons/sec (DCF eval, n=32)",
+        "value": value, "unit": "comparisons/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"DCF eval n=32 out_bits=32, 2^{args.log2n} keys per GPU, "
+                               "both parties per step, keys resident in HBM",
+                   "global_batch": ws * N, "seq_len": None, "parallelism": f"dp{ws} (element shards)",
+                   "l2": "inputs larger than L2 (18 GB of keys per GPU)"},
+        "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved_gbs / hbm_peak,
+                     "traffic": (traffic * N if traffic else None),
+                     "note": "kernel dcf_eval_kernel; 1096 algorithmic B per party-eval; the "
+                             "binding roof is compute_roofline (shared-memory T-table lookups)"},
+        "compute_roofline": {"bound": "smem-lookup", "achieved": aes_rate, "peak": aes_peak,
+                             "unit": "AES-blocks/s", "frac": aes_rate / aes_peak,
+                             "note": f"{AES_PER_EVAL} AES/party-eval, {LDS_PER_AES} LDS/AES, "
+                                     f"{LDS_PER_CLK_SM} LDS/clk/SM x {sms} SMs x {sm_max:.0f} MHz"},
+        "kernel_ms_per_launch": avg_launch_s * 1e3,
+        "clocks": clocks,
+        "gpu_launches": 2 * args.steps,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = _args()
+    ws, rank, local = _dist()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    run_ours(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

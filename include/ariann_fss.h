@@ -1,0 +1,120 @@
+/*
+ * ariann_fss.h -- C ABI of the B200 (sm_100a) FSS hot path.
+ *
+ * Drop-in boundary for AriaNN's function-secret-sharing path
+ * (reference: /root/reference/pkg/src/ariann/{prg,fss}.py). The reference is
+ * pure Python + numpy, so its "FFI" is the Python module surface; each entry
+ * point below replaces the body of one reference function and is bound from
+ * Python with ctypes (paper_2006_04593_b200/_lib.py).
+ *
+ * Conventions
+ *   - Every pointer is a DEVICE pointer (caller-owned; the library never keeps
+ *     it after return). Layouts are the reference's in-memory struct-of-arrays
+ *     layout (fss.py:71-154): seeds (count,16) u8; scw (n,ld,16) u8; tcw (n,ld)
+ *     u8; sigma_cw (n,ld) u64; leaf_cw (n+1,ld) u64; ring values u64 masked to
+ *     their ring width. `ld` is the element stride between levels (== count for
+ *     a freshly generated batch, larger for a column slice of a bigger batch).
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream). Calls are
+ *     asynchronous and reentrant; there is no global mutable state except the
+ *     thread-local error string.
+ *   - Return 0 on success; FSS_EINVAL (-> Python ValueError) or FSS_ECUDA
+ *     (-> RuntimeError); fss_last_error() gives the calling thread's message.
+ */
+#ifndef ARIANN_FSS_H
+#define ARIANN_FSS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSS_ABI_VERSION 1
+#define FSS_OK 0
+#define FSS_EINVAL 1
+#define FSS_ECUDA 2
+
+/* numpy PCG64 bit-generator state (Generator.bit_generator.state) */
+typedef struct {
+    uint64_t state_lo, state_hi; /* 128-bit LCG state */
+    uint64_t inc_lo, inc_hi;     /* 128-bit increment */
+    int32_t has_uint32;          /* buffered 32-bit half-word present */
+    uint32_t uinteger;           /* the buffered half-word */
+    uint64_t advance;            /* out: 64-bit outputs consumed */
+} fss_pcg64_state;
+
+const char* fss_last_error(void);
+int fss_abi_version(void);
+
+/* prg.expand (prg.py:43-60): out[e, 16b:16b+16] = AES_{k_b}(seeds[e]) ^ seeds[e],
+ * b < out_blocks in {2,3}; seeds are used as given (top bit not cleared). */
+int fss_aes_mmo_expand(const uint8_t* seeds, uint64_t count, int out_blocks, uint8_t* out,
+                       void* stream);
+
+/* fss._sample_tape (fss.py:292-303) through numpy's PCG64 Generator
+ * (_uniform_ring fss.py:47-51, random_seeds prg.py:36-40) for 1 <= n <= 63:
+ * draws alpha (if draw_alpha), alpha0, s0, s1 exactly as numpy would from `st`.
+ * st_out receives the number of 64-bit outputs consumed (`advance`) and the
+ * resulting has_uint32 flag; the caller advances its generator accordingly. */
+int fss_pcg64_tape(const fss_pcg64_state* st, int n, uint64_t count, int draw_alpha,
+                   uint64_t* alpha, uint64_t* alpha0, uint8_t* s0, uint8_t* s1,
+                   fss_pcg64_state* st_out, void* stream);
+
+/* fss._keygen_eq_core (fss.py:173-216). Outputs are level-major with ld=count. */
+int fss_dpf_keygen(int n, uint64_t count, const uint64_t* alpha, const uint64_t* alpha0,
+                   const uint8_t* s0, const uint8_t* s1, uint8_t* scw, uint8_t* tcw,
+                   uint64_t* cw_final, uint64_t* alpha1, void* stream);
+
+/* fss._keygen_cmp_core (fss.py:219-289); n <= out_bits <= 63. */
+int fss_dcf_keygen(int n, int out_bits, uint64_t count, const uint64_t* alpha,
+                   const uint64_t* alpha0, const uint8_t* s0, const uint8_t* s1, uint8_t* scw,
+                   uint8_t* tcw, uint64_t* sigma_cw, uint64_t* leaf_cw, uint64_t* alpha1,
+                   void* stream);
+
+/* fss.eval_eq (fss.py:357-377); x reduced mod 2^n inside. */
+int fss_dpf_eval(int party, int n, uint64_t count, uint64_t ld, const uint8_t* seed0,
+                 const uint8_t* scw, const uint8_t* tcw, const uint64_t* cw_final, const uint64_t* x,
+                 uint64_t* out, void* stream);
+
+/* fss.eval_cmp (fss.py:380-426); levels (n+1,count) may be NULL (return_levels). */
+int fss_dcf_eval(int party, int n, int out_bits, uint64_t count, uint64_t ld, const uint8_t* seed0,
+                 const uint8_t* scw, const uint8_t* tcw, const uint64_t* sigma_cw,
+                 const uint64_t* leaf_cw, const uint64_t* x, uint64_t* out, uint64_t* levels,
+                 void* stream);
+
+/* ARNK per-party payloads (LAYOUT.md:48-71; fss._pack_eq/_pack_cmp fss.py:540-583,
+ * _unpack_eq/_unpack_cmp fss.py:553-602). kind 0 = equality, 1 = comparison.
+ * payload is count * fss_arnk_elem_bytes(kind, n) bytes, element-major.
+ * Pack reads level rows with stride ld; unpack writes ld = count.
+ * Unused pointers (cw_final for cmp, sigma/leaf for eq) may be NULL. */
+uint64_t fss_arnk_elem_bytes(int kind, int n);
+int fss_arnk_pack(int kind, int n, uint64_t count, uint64_t ld, const uint64_t* alpha_share,
+                  const uint8_t* seed0, const uint8_t* scw, const uint8_t* tcw,
+                  const uint64_t* cw_final, const uint64_t* sigma_cw, const uint64_t* leaf_cw,
+                  uint8_t* payload, void* stream);
+int fss_arnk_unpack(int kind, int n, uint64_t count, const uint8_t* payload, uint64_t* alpha_share,
+                    uint8_t* seed0, uint8_t* scw, uint8_t* tcw, uint64_t* cw_final,
+                    uint64_t* sigma_cw, uint64_t* leaf_cw, void* stream);
+
+/* Elementwise ring arithmetic mod 2^n_bits (ring.py:99-129): out = op(a, b) & mask,
+ * b == NULL uses b_scalar. NEG / MASK ignore b. out may alias a or b. */
+#define FSS_RING_ADD 0
+#define FSS_RING_SUB 1
+#define FSS_RING_MUL 2
+#define FSS_RING_NEG 3
+#define FSS_RING_MASK 4
+int fss_ring_op(int op, int n_bits, uint64_t count, const uint64_t* a, const uint64_t* b,
+                uint64_t b_scalar, uint64_t* out, void* stream);
+
+/* Elementwise Beaver product share (beaver.py:257-294 with OP_MUL): delta/eps are
+ * opened from own+peer masked shares, z = delta*b + a*eps + c (+ delta*eps, party 0). */
+int fss_beaver_mul(int party, int n_bits, uint64_t count, const uint64_t* delta_own,
+                   const uint64_t* delta_peer, const uint64_t* eps_own, const uint64_t* eps_peer,
+                   const uint64_t* a, const uint64_t* b, const uint64_t* c, uint64_t* z,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ARIANN_FSS_H */

@@ -1,0 +1,83 @@
+"""ctypes binding of the C ABI in include/ariann_fss.h (libariann_fss.so).
+
+The library is the product path: there is no CPU fallback. Importing the
+package on a machine without the built library, or calling a compute entry
+point without a CUDA device, raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from ._build import LIB, up_to_date
+
+FSS_OK, FSS_EINVAL, FSS_ECUDA = 0, 1, 2
+
+_u8p = ctypes.c_void_p
+_vp = ctypes.c_void_p
+_u64 = ctypes.c_uint64
+_int = ctypes.c_int
+
+
+class PcgState(ctypes.Structure):
+    _fields_ = [("state_lo", ctypes.c_uint64), ("state_hi", ctypes.c_uint64),
+                ("inc_lo", ctypes.c_uint64), ("inc_hi", ctypes.c_uint64),
+                ("has_uint32", ctypes.c_int32), ("uinteger", ctypes.c_uint32),
+                ("advance", ctypes.c_uint64)]
+
+
+# name -> argtypes (all return int status unless listed in _RESTYPE)
+SIGNATURES = {
+    "fss_abi_version": [],
+    "fss_last_error": [],
+    "fss_aes_mmo_expand": [_vp, _u64, _int, _vp, _vp],
+    "fss_pcg64_tape": [ctypes.POINTER(PcgState), _int, _u64, _int, _vp, _vp, _vp, _vp,
+                       ctypes.POINTER(PcgState), _vp],
+    "fss_dpf_keygen": [_int, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "fss_dcf_keygen": [_int, _int, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "fss_dpf_eval": [_int, _int, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "fss_dcf_eval": [_int, _int, _int, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "fss_arnk_elem_bytes": [_int, _int],
+    "fss_arnk_pack": [_int, _int, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "fss_arnk_unpack": [_int, _int, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "fss_ring_op": [_int, _int, _u64, _vp, _vp, _u64, _vp, _vp],
+    "fss_beaver_mul": [_int, _int, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+}
+_RESTYPE = {"fss_last_error": ctypes.c_char_p, "fss_arnk_elem_bytes": ctypes.c_uint64}
+
+_lib = None
+
+
+def load():
+    """Load (never silently rebuild) the in-tree CUDA library."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise ImportError(
+                f"{LIB} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(the FSS path has no CPU fallback)")
+        lib = ctypes.CDLL(LIB)
+        for name, argtypes in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = argtypes
+            fn.restype = _RESTYPE.get(name, ctypes.c_int)
+        _lib = lib
+    return _lib
+
+
+def stale() -> bool:
+    return not up_to_date()
+
+
+def check(rc: int, what: str):
+    if rc == FSS_OK:
+        return
+    msg = (load().fss_last_error() or b"").decode(errors="replace")
+    if rc == FSS_EINVAL:
+        raise ValueError(f"{what}: {msg}")
+    raise RuntimeError(f"{what}: CUDA error: {msg}")
+
+
+def call(name: str, *args):
+    check(getattr(load(), name)(*args), name)

@@ -1,0 +1,118 @@
+// AES-128 (fixed MMO keys) on sm_100a: T-tables in shared memory, one lane
+// replica per bank so every lookup of a warp is bank-conflict free.
+//
+// Shared-memory layout (128 KiB, one CTA per SM):
+//   byte address = region*64K + x*256 + tsel*128 + lane*4,   x = table index byte
+//   region 0 holds Te0 (tsel 0) and Te1 (tsel 1), region 1 holds Te2 / Te3,
+//   Te_j[x] = rotl(Te0[x], 8j).
+// Lane l always hits bank l, so a warp's 32 random lookups cost one wavefront.
+// The address of a lookup is ONE PRMT: byte k of the state column goes to
+// address byte 1, the lane/table offset (lo0 = 4*lane, lo1 = 4*lane + 128) to
+// address byte 0, and zero bytes of lo* fill bytes 2..3.
+//
+// Round keys of the three fixed cipher keys (reference prg.py:24-28) are
+// compile-time constants (aes_consts.h), so AddRoundKey folds into LOP3
+// immediates. For the tree walk the key of the selected child block depends on
+// a per-element input bit; a per-thread mask m (0 or ~0) selects
+// rk = RK1 ^ (m & (RK1 ^ RK2)) -- one extra LOP3 per column.
+#pragma once
+#include <stdint.h>
+#include "aes_consts.h"
+
+namespace fssb {
+
+constexpr int kTableWords = 32768;            // 4 tables x 256 entries x 32 lanes
+constexpr int kTableBytes = kTableWords * 4;  // 128 KiB dynamic shared memory
+constexpr uint32_t kRegion1 = 65536;
+
+struct U4 {
+    uint32_t x, y, z, w;
+};
+
+// Fill the replicated tables (once per CTA; kernels are persistent).
+__device__ __forceinline__ void fill_tables(uint32_t* tab) {
+    for (int idx = threadIdx.x; idx < kTableWords; idx += blockDim.x) {
+        const int tsel = (idx >> 5) & 1;
+        const int x = (idx >> 6) & 255;
+        const int region = idx >> 14;
+        const uint32_t v = kTe0[x];
+        tab[idx] = __funnelshift_l(v, v, 8 * (2 * region + tsel));
+    }
+}
+
+struct Tab {
+    const unsigned char* base;  // shared-memory table base
+    uint32_t lo0, lo1;          // 4*lane and 4*lane+128
+};
+
+__device__ __forceinline__ Tab make_tab(const uint32_t* tab) {
+    Tab t;
+    t.base = reinterpret_cast<const unsigned char*>(tab);
+    const uint32_t lane = threadIdx.x & 31;
+    t.lo0 = lane * 4;
+    t.lo1 = lane * 4 + 128;
+    return t;
+}
+
+// Table J (0..3) looked up at byte K (0..3) of column c.
+template <int J, int K>
+__device__ __forceinline__ uint32_t T(const Tab& tb, uint32_t c) {
+    const uint32_t addr = __byte_perm(c, (J & 1) ? tb.lo1 : tb.lo0, 0x5504 + 0x10 * K);
+    return *reinterpret_cast<const uint32_t*>(tb.base + (J >> 1) * kRegion1 + addr);
+}
+
+// Round-key word w for a fixed key KEY (0..2), or for the key selected per
+// element between KEY=0 (k1, m=0) and KEY=1 (k2, m=~0) when SEL.
+template <int KEY, bool SEL>
+__device__ __forceinline__ uint32_t rk(int w, uint32_t m) {
+    if (SEL) return kRK[0][w] ^ (m & (kRK[0][w] ^ kRK[1][w]));
+    return kRK[KEY][w];
+}
+
+// One full AES-128 encryption of (c0..c3) (little-endian column words).
+template <int KEY, bool SEL>
+__device__ __forceinline__ U4 aes128(const Tab& tb, U4 s, uint32_t m) {
+    uint32_t c0 = s.x ^ rk<KEY, SEL>(0, m);
+    uint32_t c1 = s.y ^ rk<KEY, SEL>(1, m);
+    uint32_t c2 = s.z ^ rk<KEY, SEL>(2, m);
+    uint32_t c3 = s.w ^ rk<KEY, SEL>(3, m);
+#pragma unroll
+    for (int r = 1; r < 10; r++) {
+        const uint32_t n0 = T<0, 0>(tb, c0) ^ T<1, 1>(tb, c1) ^ T<2, 2>(tb, c2) ^ T<3, 3>(tb, c3) ^
+                            rk<KEY, SEL>(4 * r + 0, m);
+        const uint32_t n1 = T<0, 0>(tb, c1) ^ T<1, 1>(tb, c2) ^ T<2, 2>(tb, c3) ^ T<3, 3>(tb, c0) ^
+                            rk<KEY, SEL>(4 * r + 1, m);
+        const uint32_t n2 = T<0, 0>(tb, c2) ^ T<1, 1>(tb, c3) ^ T<2, 2>(tb, c0) ^ T<3, 3>(tb, c1) ^
+                            rk<KEY, SEL>(4 * r + 2, m);
+        const uint32_t n3 = T<0, 0>(tb, c3) ^ T<1, 1>(tb, c0) ^ T<2, 2>(tb, c1) ^ T<3, 3>(tb, c2) ^
+                            rk<KEY, SEL>(4 * r + 3, m);
+        c0 = n0;
+        c1 = n1;
+        c2 = n2;
+        c3 = n3;
+    }
+    // Last round: SubBytes+ShiftRows only. S(x) sits in byte r of Te_{(r+2)&3}[x].
+    U4 o;
+#define FSSB_LAST(a, b, c, d)                                                        \
+    __byte_perm(__byte_perm(T<2, 0>(tb, a), T<3, 1>(tb, b), 0x3250),                 \
+                __byte_perm(T<0, 2>(tb, c), T<1, 3>(tb, d), 0x7210), 0x7610)
+    o.x = FSSB_LAST(c0, c1, c2, c3) ^ rk<KEY, SEL>(40, m);
+    o.y = FSSB_LAST(c1, c2, c3, c0) ^ rk<KEY, SEL>(41, m);
+    o.z = FSSB_LAST(c2, c3, c0, c1) ^ rk<KEY, SEL>(42, m);
+    o.w = FSSB_LAST(c3, c0, c1, c2) ^ rk<KEY, SEL>(43, m);
+#undef FSSB_LAST
+    return o;
+}
+
+// Matyas-Meyer-Oseas block: AES_k(s) XOR s  (reference prg.expand, prg.py:43-60).
+template <int KEY, bool SEL>
+__device__ __forceinline__ U4 mmo(const Tab& tb, U4 s, uint32_t m) {
+    U4 o = aes128<KEY, SEL>(tb, s, m);
+    o.x ^= s.x;
+    o.y ^= s.y;
+    o.z ^= s.z;
+    o.w ^= s.w;
+    return o;
+}
+
+}  // namespace fssb

@@ -1,0 +1,532 @@
+// B200 (sm_100a) kernels for AriaNN's FSS hot path and the C-ABI that exposes
+// them (declared in include/ariann_fss.h).
+//
+// One thread walks the n tree levels of one element; seed / control bits stay
+// in registers. Correction words are stored level-major (struct of arrays,
+// exactly the reference's in-memory layout, fss.py:71-154), so at every level
+// a warp reads 32 consecutive 16-byte scw words (512 B, one coalesced LDG.128
+// per lane) plus 8-byte sigma/leaf words. Grids are persistent: one 512-thread
+// CTA per SM (the 128 KiB T-tables limit residency to one CTA), grid-striding
+// over elements.
+//
+// Evaluation computes only the AES blocks the output depends on: the block of
+// the child selected by the public input bit (key k1 or k2 chosen per element)
+// and, for comparison, the sigma/tau block (k3). The reference expands 2 (eq)
+// or 3 (cmp) blocks per level (fss.py:365, 395); the outputs are identical.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/ariann_fss.h"
+#include "aes_ttable.cuh"
+#include "common.cuh"
+
+using fssb::U4;
+
+namespace {
+
+constexpr int kThreads = 512;
+
+__device__ __forceinline__ uint64_t ring_mask(int w) { return w >= 64 ? ~0ULL : ((1ULL << w) - 1); }
+
+__device__ __forceinline__ U4 ld16(const uint8_t* p) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+    return U4{v.x, v.y, v.z, v.w};
+}
+
+__device__ __forceinline__ void st16(uint8_t* p, U4 v) {
+    *reinterpret_cast<uint4*>(p) = make_uint4(v.x, v.y, v.z, v.w);
+}
+
+__device__ __forceinline__ uint64_t lo64(U4 v) { return (uint64_t)v.x | ((uint64_t)v.y << 32); }
+__device__ __forceinline__ uint64_t hi64(U4 v) { return (uint64_t)v.z | ((uint64_t)v.w << 32); }
+
+__device__ __forceinline__ U4 xor4(U4 a, U4 b) { return U4{a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w}; }
+__device__ __forceinline__ U4 and4(U4 a, uint32_t m) { return U4{a.x & m, a.y & m, a.z & m, a.w & m}; }
+__device__ __forceinline__ U4 sel4(bool c, U4 a, U4 b) {
+    return U4{c ? a.x : b.x, c ? a.y : b.y, c ? a.z : b.z, c ? a.w : b.w};
+}
+
+// ------------------------------------------------------------------ expand
+// prg.expand (prg.py:43-60): out block b = AES_{k_b}(seed) ^ seed.
+__global__ void __launch_bounds__(kThreads, 1)
+expand_kernel(const uint8_t* __restrict__ seeds, uint64_t count, int blocks, uint8_t* __restrict__ out) {
+    extern __shared__ uint32_t tab[];
+    fssb::fill_tables(tab);
+    __syncthreads();
+    const fssb::Tab tb = fssb::make_tab(tab);
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const U4 s = ld16(seeds + 16 * e);
+        uint8_t* o = out + e * 16 * blocks;
+        st16(o, fssb::mmo<0, false>(tb, s, 0));
+        st16(o + 16, fssb::mmo<1, false>(tb, s, 0));
+        if (blocks == 3) st16(o + 32, fssb::mmo<2, false>(tb, s, 0));
+    }
+}
+
+// ---------------------------------------------------------------- DPF eval
+// fss.eval_eq (fss.py:357-377): t0 = party, per level expand, correct with
+// scw/tcw when t, descend to child x_i (MSB first); out = t*cw_final + s2r(s).
+__global__ void __launch_bounds__(kThreads, 1)
+dpf_eval_kernel(int party, int n, uint64_t count, uint64_t ld, const uint8_t* __restrict__ seed0,
+                const uint8_t* __restrict__ scw, const uint8_t* __restrict__ tcw,
+                const uint64_t* __restrict__ cw_final, const uint64_t* __restrict__ x,
+                uint64_t* __restrict__ out) {
+    extern __shared__ uint32_t tab[];
+    fssb::fill_tables(tab);
+    __syncthreads();
+    const fssb::Tab tb = fssb::make_tab(tab);
+    const uint64_t mask = ring_mask(n);
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        U4 s = ld16(seed0 + 16 * e);
+        uint32_t t = party;
+        const uint64_t xe = x[e] & mask;
+        for (int i = 0; i < n; i++) {
+            const uint64_t off = (uint64_t)i * ld + e;
+            const U4 cw = ld16(scw + 16 * off);
+            const uint32_t f = __ldg(tcw + off);
+            const uint32_t xb = (uint32_t)(xe >> (n - 1 - i)) & 1u;
+            const U4 a = fssb::mmo<0, true>(tb, s, 0u - xb);
+            const uint32_t tm = 0u - t;
+            s = xor4(a, and4(cw, tm));
+            const uint32_t tn = ((a.w >> 31) ^ (t & (f >> xb))) & 1u;
+            s.w &= 0x7FFFFFFFu;
+            t = tn;
+        }
+        uint64_t o = (((uint64_t)t * cw_final[e]) + lo64(s)) & mask;
+        if (party) o = (0 - o) & mask;
+        out[e] = o;
+    }
+}
+
+// ---------------------------------------------------------------- DCF eval
+// fss.eval_cmp (fss.py:380-426). Per level: child block (key k1/k2 by x_i) and
+// the sigma/tau block (k3, lane x_i). out_i = tau*leaf[i] + sigma (mod 2^w).
+__global__ void __launch_bounds__(kThreads, 1)
+dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
+                const uint8_t* __restrict__ seed0, const uint8_t* __restrict__ scw,
+                const uint8_t* __restrict__ tcw, const uint64_t* __restrict__ sigma_cw,
+                const uint64_t* __restrict__ leaf_cw, const uint64_t* __restrict__ x,
+                uint64_t* __restrict__ out, uint64_t* __restrict__ levels) {
+    extern __shared__ uint32_t tab[];
+    fssb::fill_tables(tab);
+    __syncthreads();
+    const fssb::Tab tb = fssb::make_tab(tab);
+    const uint64_t nmask = ring_mask(n);
+    const uint64_t mask = ring_mask(out_bits);
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        U4 s = ld16(seed0 + 16 * e);
+        uint32_t t = party;
+        uint64_t acc = 0;
+        const uint64_t xe = x[e] & nmask;
+        for (int i = 0; i < n; i++) {
+            const uint64_t off = (uint64_t)i * ld + e;
+            const U4 cw = ld16(scw + 16 * off);
+            const uint32_t f = __ldg(tcw + off);
+            const uint64_t sig = __ldg(sigma_cw + off);
+            const uint64_t leaf = __ldg(leaf_cw + off);
+            const uint32_t xb = (uint32_t)(xe >> (n - 1 - i)) & 1u;
+            const U4 a = fssb::mmo<0, true>(tb, s, 0u - xb);
+            const U4 g = fssb::mmo<2, false>(tb, s, 0);
+            const uint32_t tm = 0u - t;
+            // sigma/tau lane x_i of the third block (slice_cmp, prg.py:99-119)
+            const uint64_t lane = xb ? hi64(g) : lo64(g);
+            const uint32_t tau = ((uint32_t)(lane >> 63) ^ (t & (f >> (2 + xb)))) & 1u;
+            const uint64_t sigma = (lane & mask) ^ (sig & (0ULL - (uint64_t)t));
+            const uint64_t oi = (((uint64_t)tau * leaf) + sigma) & mask;
+            acc = (acc + oi) & mask;
+            if (levels) levels[(uint64_t)i * count + e] = party ? ((0 - oi) & mask) : oi;
+            s = xor4(a, and4(cw, tm));
+            const uint32_t tn = ((a.w >> 31) ^ (t & (f >> xb))) & 1u;
+            s.w &= 0x7FFFFFFFu;
+            t = tn;
+        }
+        const uint64_t off = (uint64_t)n * ld + e;
+        const uint64_t last = (((uint64_t)t * __ldg(leaf_cw + off)) + lo64(s)) & mask;
+        acc = (acc + last) & mask;
+        if (levels) levels[(uint64_t)n * count + e] = party ? ((0 - last) & mask) : last;
+        out[e] = party ? ((0 - acc) & mask) : acc;
+    }
+}
+
+// -------------------------------------------------------------- DPF keygen
+// fss._keygen_eq_core (fss.py:173-216): both parties' walks, 4 AES blocks/level.
+__global__ void __launch_bounds__(kThreads, 1)
+dpf_keygen_kernel(int n, uint64_t count, const uint64_t* __restrict__ alpha,
+                  const uint64_t* __restrict__ alpha0, const uint8_t* __restrict__ s0_init,
+                  const uint8_t* __restrict__ s1_init, uint8_t* __restrict__ scw,
+                  uint8_t* __restrict__ tcw, uint64_t* __restrict__ cw_final,
+                  uint64_t* __restrict__ alpha1) {
+    extern __shared__ uint32_t tab[];
+    fssb::fill_tables(tab);
+    __syncthreads();
+    const fssb::Tab tb = fssb::make_tab(tab);
+    const uint64_t mask = ring_mask(n);
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        U4 s0 = ld16(s0_init + 16 * e), s1 = ld16(s1_init + 16 * e);
+        uint32_t t0 = 0, t1 = 1;
+        const uint64_t al = alpha[e] & mask;
+        for (int i = 0; i < n; i++) {
+            const uint32_t a = (uint32_t)(al >> (n - 1 - i)) & 1u;
+            U4 l0 = fssb::mmo<0, false>(tb, s0, 0), r0 = fssb::mmo<1, false>(tb, s0, 0);
+            U4 l1 = fssb::mmo<0, false>(tb, s1, 0), r1 = fssb::mmo<1, false>(tb, s1, 0);
+            const uint32_t tl0 = l0.w >> 31, tr0 = r0.w >> 31, tl1 = l1.w >> 31, tr1 = r1.w >> 31;
+            l0.w &= 0x7FFFFFFFu; r0.w &= 0x7FFFFFFFu; l1.w &= 0x7FFFFFFFu; r1.w &= 0x7FFFFFFFu;
+            // seed correction reuses the off-path child's string
+            const U4 cws = a ? xor4(l0, l1) : xor4(r0, r1);
+            const uint32_t cw_tl = tl0 ^ tl1 ^ 1u ^ a;
+            const uint32_t cw_tr = tr0 ^ tr1 ^ a;
+            const uint64_t off = (uint64_t)i * count + e;
+            st16(scw + 16 * off, cws);
+            tcw[off] = (uint8_t)(cw_tl | (cw_tr << 1));
+            // advance both parties along alpha
+            s0 = xor4(sel4(a, r0, l0), and4(cws, 0u - t0));
+            s1 = xor4(sel4(a, r1, l1), and4(cws, 0u - t1));
+            const uint32_t n0 = (a ? tr0 : tl0) ^ (t0 & (a ? cw_tr : cw_tl));
+            const uint32_t n1 = (a ? tr1 : tl1) ^ (t1 & (a ? cw_tr : cw_tl));
+            t0 = n0;
+            t1 = n1;
+        }
+        const uint64_t v = (1 - lo64(s0) + lo64(s1)) & mask;
+        cw_final[e] = t1 ? ((0 - v) & mask) : v;
+        alpha1[e] = (al - alpha0[e]) & mask;
+    }
+}
+
+// -------------------------------------------------------------- DCF keygen
+// fss._keygen_cmp_core (fss.py:219-289): 6 AES blocks/level (3 per party).
+__global__ void __launch_bounds__(kThreads, 1)
+dcf_keygen_kernel(int n, int out_bits, uint64_t count, const uint64_t* __restrict__ alpha,
+                  const uint64_t* __restrict__ alpha0, const uint8_t* __restrict__ s0_init,
+                  const uint8_t* __restrict__ s1_init, uint8_t* __restrict__ scw,
+                  uint8_t* __restrict__ tcw, uint64_t* __restrict__ sigma_cw,
+                  uint64_t* __restrict__ leaf_cw, uint64_t* __restrict__ alpha1) {
+    extern __shared__ uint32_t tab[];
+    fssb::fill_tables(tab);
+    __syncthreads();
+    const fssb::Tab tb = fssb::make_tab(tab);
+    const uint64_t nmask = ring_mask(n);
+    const uint64_t mask = ring_mask(out_bits);
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        U4 s0 = ld16(s0_init + 16 * e), s1 = ld16(s1_init + 16 * e);
+        uint32_t t0 = 0, t1 = 1;
+        const uint64_t al = alpha[e] & nmask;
+        for (int i = 0; i < n; i++) {
+            const uint32_t a = (uint32_t)(al >> (n - 1 - i)) & 1u;
+            U4 l0 = fssb::mmo<0, false>(tb, s0, 0), r0 = fssb::mmo<1, false>(tb, s0, 0);
+            const U4 g0 = fssb::mmo<2, false>(tb, s0, 0);
+            U4 l1 = fssb::mmo<0, false>(tb, s1, 0), r1 = fssb::mmo<1, false>(tb, s1, 0);
+            const U4 g1 = fssb::mmo<2, false>(tb, s1, 0);
+            const uint32_t tl0 = l0.w >> 31, tr0 = r0.w >> 31, tl1 = l1.w >> 31, tr1 = r1.w >> 31;
+            l0.w &= 0x7FFFFFFFu; r0.w &= 0x7FFFFFFFu; l1.w &= 0x7FFFFFFFu; r1.w &= 0x7FFFFFFFu;
+            const uint64_t gl0 = lo64(g0) & mask, gr0 = hi64(g0) & mask;
+            const uint64_t gl1 = lo64(g1) & mask, gr1 = hi64(g1) & mask;
+            const uint32_t ul0 = g0.y >> 31, ur0 = g0.w >> 31, ul1 = g1.y >> 31, ur1 = g1.w >> 31;
+
+            const U4 cws = a ? xor4(l0, l1) : xor4(r0, r1);
+            const uint32_t cw_tl = tl0 ^ tl1 ^ 1u ^ a;
+            const uint32_t cw_tr = tr0 ^ tr1 ^ a;
+            // sigma collapses on the stay side (alpha bit), fss.py:245-249
+            const uint64_t cw_sig = a ? (gr0 ^ gr1) : (gl0 ^ gl1);
+            const uint32_t cw_ul = ul0 ^ ul1 ^ a;
+            const uint32_t cw_ur = ur0 ^ ur1 ^ 1u ^ a;
+            const uint64_t off = (uint64_t)i * count + e;
+            st16(scw + 16 * off, cws);
+            tcw[off] = (uint8_t)(cw_tl | (cw_tr << 1) | (cw_ul << 2) | (cw_ur << 3));
+            sigma_cw[off] = cw_sig;
+            // leaf word from the exit side (not alpha bit) after correction, fss.py:268-273
+            const uint64_t g0x = (a ? gl0 : gr0) ^ (t0 ? cw_sig : 0);
+            const uint64_t g1x = (a ? gl1 : gr1) ^ (t1 ? cw_sig : 0);
+            const uint32_t u1x = (a ? ul1 : ur1) ^ (t1 & (a ? cw_ul : cw_ur));
+            const uint64_t leaf = ((uint64_t)a - g0x + g1x) & mask;
+            leaf_cw[off] = u1x ? ((0 - leaf) & mask) : leaf;
+            // advance along alpha
+            s0 = xor4(sel4(a, r0, l0), and4(cws, 0u - t0));
+            s1 = xor4(sel4(a, r1, l1), and4(cws, 0u - t1));
+            const uint32_t n0 = (a ? tr0 : tl0) ^ (t0 & (a ? cw_tr : cw_tl));
+            const uint32_t n1 = (a ? tr1 : tl1) ^ (t1 & (a ? cw_tr : cw_tl));
+            t0 = n0;
+            t1 = n1;
+        }
+        const uint64_t v = (1 - (lo64(s0) & mask) + (lo64(s1) & mask)) & mask;
+        leaf_cw[(uint64_t)n * count + e] = t1 ? ((0 - v) & mask) : v;
+        alpha1[e] = (al - alpha0[e]) & nmask;
+    }
+}
+
+// ------------------------------------------------------------ PCG64 tapes
+// Device restatement of numpy's Generator(PCG64) draws behind fss._sample_tape
+// (fss.py:292-303): PCG64 XSL-RR 128/64, step-then-output. The 32-bit stream
+// splits each 64-bit output low half first (numpy next_uint32), bounded draws
+// with power-of-two ranges are word >> (32-n) (Lemire, no rejection), uint8
+// draws take the 4 bytes of each word in little-endian order.
+struct Pcg {
+    unsigned __int128 state, inc;
+};
+
+__device__ __forceinline__ unsigned __int128 pcg_mult() {
+    return ((unsigned __int128)0x2360ed051fc65da4ULL << 64) | 0x4385df649fccf645ULL;
+}
+
+__device__ __forceinline__ Pcg pcg_advance(Pcg p, uint64_t delta) {
+    unsigned __int128 cur_mult = pcg_mult(), cur_plus = p.inc, acc_mult = 1, acc_plus = 0;
+    while (delta) {
+        if (delta & 1) {
+            acc_mult *= cur_mult;
+            acc_plus = acc_plus * cur_mult + cur_plus;
+        }
+        cur_plus = (cur_mult + 1) * cur_plus;
+        cur_mult *= cur_mult;
+        delta >>= 1;
+    }
+    p.state = acc_mult * p.state + acc_plus;
+    return p;
+}
+
+__device__ __forceinline__ uint64_t pcg_next(Pcg& p) {
+    p.state = p.state * pcg_mult() + p.inc;
+    const uint64_t hi = (uint64_t)(p.state >> 64), lo = (uint64_t)p.state;
+    const uint64_t xr = hi ^ lo;
+    const unsigned rot = (unsigned)(hi >> 58);
+    return (xr >> rot) | (xr << ((64 - rot) & 63));
+}
+
+struct TapePlan {
+    uint64_t state_lo, state_hi, inc_lo, inc_hi;
+    int n;
+    uint64_t count;
+    int draw_alpha;    // alpha drawn (1) or given (0)
+    int has_uint32;    // numpy's buffered half-word present at start
+    uint32_t uinteger;
+    uint64_t raw64;    // number of 64-bit draws before the 32-bit stream (n > 32)
+    uint64_t words;    // number of 32-bit words in the stream
+};
+
+// Thread j handles raw outputs [j*kChunk, (j+1)*kChunk).
+constexpr int kChunk = 16;
+
+__device__ __forceinline__ void emit_word(const TapePlan& P, uint64_t w, uint32_t v, uint64_t* alpha,
+                                          uint64_t* alpha0, uint8_t* s0, uint8_t* s1) {
+    const uint64_t N = P.count;
+    uint64_t k = w;
+    if (P.n <= 32) {
+        const int sh = 32 - P.n;
+        if (P.draw_alpha) {
+            if (k < N) { alpha[k] = (uint64_t)(v >> sh); return; }
+            k -= N;
+        }
+        if (k < N) { alpha0[k] = (uint64_t)(v >> sh); return; }
+        k -= N;
+    }
+    // seeds: 4 words per seed, byte 15 top bit cleared (prg.random_seeds, prg.py:36-40)
+    uint8_t* dst = k < 4 * N ? s0 : s1;
+    if (k >= 4 * N) k -= 4 * N;
+    if ((k & 3) == 3) v &= 0x7FFFFFFFu;
+    reinterpret_cast<uint32_t*>(dst)[k] = v;
+}
+
+__global__ void pcg64_tape_kernel(TapePlan P, uint64_t* __restrict__ alpha, uint64_t* __restrict__ alpha0,
+                                  uint8_t* __restrict__ s0, uint8_t* __restrict__ s1) {
+    const uint64_t h = (uint64_t)P.has_uint32;
+    const uint64_t raw_words = (P.words - h + 1) / 2;     // 64-bit draws feeding the word stream
+    const uint64_t total = P.raw64 + raw_words;
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j == 0 && h && P.words > 0) emit_word(P, 0, P.uinteger, alpha, alpha0, s0, s1);
+    const uint64_t begin = j * kChunk;
+    if (begin >= total) return;
+    const uint64_t end = begin + kChunk < total ? begin + kChunk : total;
+    Pcg p;
+    p.state = ((unsigned __int128)P.state_hi << 64) | P.state_lo;
+    p.inc = ((unsigned __int128)P.inc_hi << 64) | P.inc_lo;
+    p = pcg_advance(p, begin);
+    const uint64_t N = P.count;
+    const int sh64 = 64 - P.n;
+    for (uint64_t r = begin; r < end; r++) {
+        const uint64_t v = pcg_next(p);
+        if (r < P.raw64) {  // n > 32: 64-bit Lemire draws, v >> (64-n)
+            uint64_t k = r;
+            if (P.draw_alpha) {
+                if (k < N) { alpha[k] = v >> sh64; continue; }
+                k -= N;
+            }
+            alpha0[k] = v >> sh64;
+            continue;
+        }
+        const uint64_t q = r - P.raw64;
+        const uint64_t w_lo = h + 2 * q, w_hi = w_lo + 1;
+        if (w_lo < P.words) emit_word(P, w_lo, (uint32_t)v, alpha, alpha0, s0, s1);
+        if (w_hi < P.words) emit_word(P, w_hi, (uint32_t)(v >> 32), alpha, alpha0, s0, s1);
+    }
+}
+
+// ------------------------------------------------------------ runtime glue
+
+constexpr int kOk = FSS_OK, kEinval = FSS_EINVAL, kEcuda = FSS_ECUDA;
+
+int set_err(int code, const char* fmt, const char* a = "") {
+    char buf[512];
+    snprintf(buf, sizeof(buf), fmt, a);
+    return fssb::set_error(code, buf);
+}
+
+struct DevInfo {
+    int sms = 0;
+    bool attr_done = false;
+};
+DevInfo g_dev[64];
+
+template <typename K>
+int prep_launch(K kernel, int* grid) {
+    int dev = 0;
+    cudaError_t err = cudaGetDevice(&dev);
+    if (err != cudaSuccess) return set_err(kEcuda, "cudaGetDevice: %s", cudaGetErrorString(err));
+    DevInfo& d = g_dev[dev & 63];
+    if (!d.sms) cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fssb::kTableBytes);
+    if (err != cudaSuccess) return set_err(kEcuda, "cudaFuncSetAttribute: %s", cudaGetErrorString(err));
+    *grid = d.sms;
+    return kOk;
+}
+
+int grid_for(uint64_t count, int sms) {
+    const uint64_t need = (count + kThreads - 1) / kThreads;
+    return (int)(need < (uint64_t)sms ? (need ? need : 1) : sms);
+}
+
+int check_launch() {
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return set_err(kEcuda, "kernel launch: %s", cudaGetErrorString(err));
+    return kOk;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fss_last_error(void) { return fssb::last_error(); }
+
+int fss_abi_version(void) { return FSS_ABI_VERSION; }
+
+int fss_aes_mmo_expand(const uint8_t* seeds, uint64_t count, int out_blocks, uint8_t* out,
+                       void* stream) {
+    if (out_blocks < 2 || out_blocks > 3) return set_err(kEinval, "out_blocks must be 2 or 3%s");
+    if (count == 0) return kOk;
+    int sms;
+    if (int rc = prep_launch(expand_kernel, &sms)) return rc;
+    expand_kernel<<<grid_for(count, sms), kThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+        seeds, count, out_blocks, out);
+    return check_launch();
+}
+
+int fss_dpf_eval(int party, int n, uint64_t count, uint64_t ld, const uint8_t* seed0,
+                 const uint8_t* scw, const uint8_t* tcw, const uint64_t* cw_final, const uint64_t* x,
+                 uint64_t* out, void* stream) {
+    if (party != 0 && party != 1) return set_err(kEinval, "party must be 0 or 1%s");
+    if (n < 1 || n > 64) return set_err(kEinval, "n out of range%s");
+    if (count == 0) return kOk;
+    int sms;
+    if (int rc = prep_launch(dpf_eval_kernel, &sms)) return rc;
+    dpf_eval_kernel<<<grid_for(count, sms), kThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+        party, n, count, ld, seed0, scw, tcw, cw_final, x, out);
+    return check_launch();
+}
+
+int fss_dcf_eval(int party, int n, int out_bits, uint64_t count, uint64_t ld, const uint8_t* seed0,
+                 const uint8_t* scw, const uint8_t* tcw, const uint64_t* sigma_cw,
+                 const uint64_t* leaf_cw, const uint64_t* x, uint64_t* out, uint64_t* levels,
+                 void* stream) {
+    if (party != 0 && party != 1) return set_err(kEinval, "party must be 0 or 1%s");
+    if (n < 1 || n > 63 || out_bits < n || out_bits > 63)
+        return set_err(kEinval, "need 1 <= n <= out_bits <= 63%s");
+    if (count == 0) return kOk;
+    int sms;
+    if (int rc = prep_launch(dcf_eval_kernel, &sms)) return rc;
+    dcf_eval_kernel<<<grid_for(count, sms), kThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+        party, n, out_bits, count, ld, seed0, scw, tcw, sigma_cw, leaf_cw, x, out, levels);
+    return check_launch();
+}
+
+int fss_dpf_keygen(int n, uint64_t count, const uint64_t* alpha, const uint64_t* alpha0,
+                   const uint8_t* s0, const uint8_t* s1, uint8_t* scw, uint8_t* tcw,
+                   uint64_t* cw_final, uint64_t* alpha1, void* stream) {
+    if (n < 1 || n > 64) return set_err(kEinval, "n out of range%s");
+    if (count == 0) return kOk;
+    int sms;
+    if (int rc = prep_launch(dpf_keygen_kernel, &sms)) return rc;
+    dpf_keygen_kernel<<<grid_for(count, sms), kThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+        n, count, alpha, alpha0, s0, s1, scw, tcw, cw_final, alpha1);
+    return check_launch();
+}
+
+int fss_dcf_keygen(int n, int out_bits, uint64_t count, const uint64_t* alpha,
+                   const uint64_t* alpha0, const uint8_t* s0, const uint8_t* s1, uint8_t* scw,
+                   uint8_t* tcw, uint64_t* sigma_cw, uint64_t* leaf_cw, uint64_t* alpha1,
+                   void* stream) {
+    if (n < 1 || n > 63 || out_bits < n || out_bits > 63)
+        return set_err(kEinval, "need 1 <= n <= out_bits <= 63%s");
+    if (count == 0) return kOk;
+    int sms;
+    if (int rc = prep_launch(dcf_keygen_kernel, &sms)) return rc;
+    dcf_keygen_kernel<<<grid_for(count, sms), kThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+        n, out_bits, count, alpha, alpha0, s0, s1, scw, tcw, sigma_cw, leaf_cw, alpha1);
+    return check_launch();
+}
+
+int fss_pcg64_tape(const fss_pcg64_state* st, int n, uint64_t count, int draw_alpha,
+                   uint64_t* alpha, uint64_t* alpha0, uint8_t* s0, uint8_t* s1,
+                   fss_pcg64_state* st_out, void* stream) {
+    if (n < 1 || n > 63) return set_err(kEinval, "device tape supports n <= 63%s");
+    TapePlan P;
+    P.state_lo = st->state_lo; P.state_hi = st->state_hi;
+    P.inc_lo = st->inc_lo; P.inc_hi = st->inc_hi;
+    P.n = n; P.count = count; P.draw_alpha = draw_alpha ? 1 : 0;
+    P.has_uint32 = st->has_uint32 ? 1 : 0;
+    P.uinteger = st->uinteger;
+    const uint64_t na = P.draw_alpha ? count : 0;
+    if (n <= 32) {
+        P.raw64 = 0;
+        P.words = na + count + 8 * count;
+    } else {
+        P.raw64 = na + count;
+        P.words = 8 * count;
+    }
+    const uint64_t h = (uint64_t)P.has_uint32;
+    const uint64_t raw_words = P.words >= h ? (P.words - h + 1) / 2 : 0;
+    const uint64_t total = P.raw64 + raw_words;
+    // host-side bookkeeping for the caller's generator: raws consumed and the
+    // buffered half-word left behind (numpy's has_uint32 / uinteger)
+    if (st_out) {
+        *st_out = *st;
+        st_out->advance = total;
+        const int used_buffer = (P.words > 0 && h);
+        const uint64_t fresh = P.words - (used_buffer ? 1 : 0);
+        st_out->has_uint32 = (P.words == 0) ? st->has_uint32 : (int)(fresh & 1);
+        st_out->uinteger = 0;  // caller fills from the last raw output when has_uint32
+    }
+    if (count == 0) return kOk;
+    const uint64_t threads = (total + kChunk - 1) / kChunk;
+    const int bs = 256;
+    const uint64_t grid = threads ? (threads + bs - 1) / bs : 1;
+    pcg64_tape_kernel<<<(unsigned)grid, bs, 0, (cudaStream_t)stream>>>(P, alpha, alpha0, s0, s1);
+    return check_launch();
+}
+
+}  // extern "C"
+
+namespace fssb {
+namespace {
+thread_local char g_err[512] = {0};
+}
+int set_error(int code, const char* msg) {
+    strncpy(g_err, msg, sizeof(g_err) - 1);
+    g_err[sizeof(g_err) - 1] = 0;
+    return code;
+}
+const char* last_error() { return g_err; }
+}  // namespace fssb

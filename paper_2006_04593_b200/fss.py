@@ -1,0 +1,734 @@
+"""Drop-in for the reference's ``ariann.fss`` (pkg/src/ariann/fss.py) on B200.
+
+Same entry points, key types (field names, shapes, dtypes) and error classes
+as the reference; key material lives in HBM as ``torch`` tensors in the
+reference's struct-of-arrays layout, and every compute step is a sm_100a
+kernel behind the C ABI (include/ariann_fss.h):
+
+  _sample_tape        -> fss_pcg64_tape   (numpy PCG64 draws reproduced on device)
+  _keygen_eq_core     -> fss_dpf_keygen
+  _keygen_cmp_core    -> fss_dcf_keygen
+  eval_eq / eval_cmp  -> fss_dpf_eval / fss_dcf_eval
+  _pack_* / _unpack_* -> fss_arnk_pack / fss_arnk_unpack
+
+Type convention: inputs given as numpy arrays / Python ints are host buffers
+(copied in, results copied back to numpy); torch CUDA tensors stay on device.
+``consumed`` bookkeeping stays a host numpy bool array (it is metadata, not key
+material). ``take`` of a contiguous index range returns zero-copy column views
+(the kernels take a level stride), other index sets are gathered on device.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _dev, _lib, prg
+from ._lib import PcgState
+from .ring import ring_mask
+
+LAMBDA = prg.SEED_BITS
+
+MAGIC = b"ARNK"
+VERSION = 1
+KIND_EQ = 0
+KIND_CMP = 1
+KIND_TRIPLE = 2
+
+_HEADER_BYTES = 13  # magic 4 | version 1 | kind 1 | n 1 | lambda 2 | count 4
+
+
+class KeyFormatError(ValueError):
+    """Malformed serialized key material."""
+
+
+class KeyExhaustedError(RuntimeError):
+    """More single-use keys requested than remain unconsumed."""
+
+
+# ---------------------------------------------------------------------------
+# Key containers (fss.py:59-166)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class FssTape:
+    """Dealer randomness disclosed for cut-and-choose auditing (fss.py:59-68)."""
+
+    alpha: torch.Tensor  # (count,) u64
+    s0: torch.Tensor     # (count, 16) u8
+    s1: torch.Tensor     # (count, 16) u8
+
+    def take(self, idx) -> "FssTape":
+        sel, _ = _index(idx, self.alpha.shape[0], self.alpha.device)
+        return FssTape(_take1(self.alpha, sel), _take1(self.s0, sel), _take1(self.s1, sel))
+
+
+def _index(idx, count: int, device):
+    """Normalise an index spec -> (slice | device LongTensor, numpy int64 indices)."""
+    if isinstance(idx, slice):
+        arr = np.arange(count)[idx]
+    elif isinstance(idx, torch.Tensor):
+        arr = idx.detach().cpu().numpy().astype(np.int64).reshape(-1)
+    else:
+        arr = np.asarray(list(idx) if isinstance(idx, range) else idx, dtype=np.int64).reshape(-1)
+    if arr.size and (arr.min() < -count or arr.max() >= count):
+        raise IndexError(f"key index out of range for a batch of {count}")
+    arr = np.where(arr < 0, arr + count, arr)
+    if arr.size == 0:
+        return slice(0, 0), arr
+    lo = int(arr[0])
+    if arr.size == 1 or np.all(np.diff(arr) == 1):
+        return slice(lo, lo + arr.size), arr
+    return torch.from_numpy(arr).to(device), arr
+
+
+def _take1(t: torch.Tensor, sel):
+    """Select along the element axis 0."""
+    if isinstance(sel, slice):
+        return t[sel]
+    return _dev.index_select(t, 0, sel)
+
+
+def _take2(t: torch.Tensor, sel):
+    """Select along the element axis 1 of a level-major array."""
+    if isinstance(sel, slice):
+        return t[:, sel]
+    return _dev.index_select(t, 1, sel)
+
+
+def _check_party_tensors(k, names):
+    dev = k.alpha_share.device
+    for name in names:
+        t = getattr(k, name)
+        if not isinstance(t, torch.Tensor):
+            raise KeyFormatError(f"{name} must be a torch tensor (device-resident key)")
+        if t.device != dev:
+            raise KeyFormatError(f"{name} lives on {t.device}, expected {dev}")
+
+
+@dataclass
+class EqKeyBatch:
+    """One party's batch of equality keys (struct-of-arrays, fss.py:71-105)."""
+
+    party: int
+    n_bits: int
+    alpha_share: torch.Tensor   # (count,) u64
+    seed0: torch.Tensor         # (count, 16) u8
+    scw: torch.Tensor           # (n, count, 16) u8 seed corrections
+    tcw: torch.Tensor           # (n, count) u8: bit0 = left t, bit1 = right t
+    cw_final: torch.Tensor      # (count,) u64
+    consumed: np.ndarray = field(default=None)
+
+    def __post_init__(self):
+        if self.consumed is None:
+            self.consumed = np.zeros(self.count, dtype=bool)
+
+    @property
+    def count(self) -> int:
+        return int(self.alpha_share.shape[0])
+
+    @property
+    def device(self):
+        return self.alpha_share.device
+
+    def validate(self):
+        n, count = self.n_bits, self.count
+        if tuple(self.scw.shape) != (n, count, 16) or tuple(self.tcw.shape) != (n, count):
+            raise KeyFormatError("correction word arrays do not match n_bits/count")
+        if tuple(self.seed0.shape) != (count, 16) or tuple(self.cw_final.shape) != (count,):
+            raise KeyFormatError("seed/final arrays do not match count")
+        _check_party_tensors(self, ("seed0", "scw", "tcw", "cw_final"))
+
+    def take(self, idx) -> "EqKeyBatch":
+        sel, arr = _index(idx, self.count, self.device)
+        return EqKeyBatch(self.party, self.n_bits, _take1(self.alpha_share, sel),
+                          _take1(self.seed0, sel), _take2(self.scw, sel), _take2(self.tcw, sel),
+                          _take1(self.cw_final, sel), self.consumed[arr].copy())
+
+    def take_unused(self, m: int) -> "EqKeyBatch":
+        return _take_unused(self, m)
+
+
+@dataclass
+class CmpKeyBatch:
+    """One party's batch of comparison keys (fss.py:108-154)."""
+
+    party: int
+    n_bits: int
+    alpha_share: torch.Tensor   # (count,) u64
+    seed0: torch.Tensor         # (count, 16) u8
+    scw: torch.Tensor           # (n, count, 16) u8
+    tcw: torch.Tensor           # (n, count) u8: bits 0..3 = tL, tR, tauL, tauR
+    sigma_cw: torch.Tensor      # (n, count) u64
+    leaf_cw: torch.Tensor       # (n+1, count) u64
+    consumed: np.ndarray = field(default=None)
+    out_bits: int = None
+
+    def __post_init__(self):
+        if self.consumed is None:
+            self.consumed = np.zeros(self.count, dtype=bool)
+        if self.out_bits is None:
+            self.out_bits = self.n_bits
+
+    @property
+    def count(self) -> int:
+        return int(self.alpha_share.shape[0])
+
+    @property
+    def device(self):
+        return self.alpha_share.device
+
+    def validate(self):
+        n, count = self.n_bits, self.count
+        if tuple(self.scw.shape) != (n, count, 16) or tuple(self.tcw.shape) != (n, count):
+            raise KeyFormatError("correction word arrays do not match n_bits/count")
+        if tuple(self.sigma_cw.shape) != (n, count) or tuple(self.leaf_cw.shape) != (n + 1, count):
+            raise KeyFormatError("sigma/leaf arrays do not match n_bits/count")
+        if tuple(self.seed0.shape) != (count, 16):
+            raise KeyFormatError("seed array does not match count")
+        _check_party_tensors(self, ("seed0", "scw", "tcw", "sigma_cw", "leaf_cw"))
+
+    def take(self, idx) -> "CmpKeyBatch":
+        sel, arr = _index(idx, self.count, self.device)
+        return CmpKeyBatch(self.party, self.n_bits, _take1(self.alpha_share, sel),
+                           _take1(self.seed0, sel), _take2(self.scw, sel), _take2(self.tcw, sel),
+                           _take2(self.sigma_cw, sel), _take2(self.leaf_cw, sel),
+                           self.consumed[arr].copy(), self.out_bits)
+
+    def take_unused(self, m: int) -> "CmpKeyBatch":
+        return _take_unused(self, m)
+
+
+def _take_unused(batch, m: int):
+    """Single-use key hand-out (fss.py:157-166)."""
+    free = np.flatnonzero(~batch.consumed)
+    if free.size < m:
+        raise KeyExhaustedError(
+            f"requested {m} keys but only {free.size} unconsumed remain (single-use)")
+    idx = free[:m]
+    out = batch.take(idx)
+    batch.consumed[idx] = True
+    out.consumed[:] = True  # the view itself is spent once handed out
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Randomness tape: numpy's Generator(PCG64) stream reproduced on device
+# ---------------------------------------------------------------------------
+
+_M64 = (1 << 64) - 1
+_M128 = (1 << 128) - 1
+_PCG_MULT = 0x2360ED051FC65DA44385DF649FCCF645
+
+
+def _pcg_jump(state: int, inc: int, delta: int) -> int:
+    acc_mult, acc_plus, cur_mult, cur_plus = 1, 0, _PCG_MULT, inc
+    while delta:
+        if delta & 1:
+            acc_mult = (acc_mult * cur_mult) & _M128
+            acc_plus = (acc_plus * cur_mult + cur_plus) & _M128
+        cur_plus = ((cur_mult + 1) * cur_plus) & _M128
+        cur_mult = (cur_mult * cur_mult) & _M128
+        delta >>= 1
+    return (acc_mult * state + acc_plus) & _M128
+
+
+def _pcg_output(state: int) -> int:
+    hi, lo = state >> 64, state & _M64
+    x, r = hi ^ lo, hi >> 58
+    return ((x >> r) | (x << ((64 - r) & 63))) & _M64
+
+
+def _device_tape_ok(n: int, rng) -> bool:
+    return (1 <= n <= 63 and isinstance(rng, np.random.Generator)
+            and type(rng.bit_generator).__name__ == "PCG64")
+
+
+def _sample_tape(n: int, rng, count: int, alpha, device):
+    """fss._sample_tape (fss.py:292-303): draw order alpha (unless given),
+    alpha0, s0, s1 -- bit-identical to the reference's numpy draws."""
+    if alpha is not None:
+        alpha_t = _dev.to_device_u64(alpha, device)
+        if tuple(alpha_t.shape) != (count,):
+            raise ValueError("alpha must have shape (count,)")
+        from . import ring_ops
+        alpha_t = ring_ops.mask(alpha_t, n)
+    if not _device_tape_ok(n, rng):
+        # n = 64 (two-call uniform draw, fss.py:48-50) or a non-PCG64 generator:
+        # the randomness source itself is host numpy, exactly the reference's calls.
+        return _sample_tape_host(n, rng, count, alpha_t if alpha is not None else None, device)
+    st = rng.bit_generator.state
+    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    cst = PcgState(s & _M64, s >> 64, inc & _M64, inc >> 64, int(st["has_uint32"]),
+                   int(st["uinteger"]) & 0xFFFFFFFF, 0)
+    out_st = PcgState()
+    draw_alpha = alpha is None
+    a = torch.empty(count, dtype=torch.uint64, device=device) if draw_alpha else alpha_t
+    a0 = torch.empty(count, dtype=torch.uint64, device=device)
+    s0 = torch.empty((count, 16), dtype=torch.uint8, device=device)
+    s1 = torch.empty((count, 16), dtype=torch.uint8, device=device)
+    with torch.cuda.device(device):
+        _lib.call("fss_pcg64_tape", cst, n, count, int(draw_alpha),
+                  _dev.ptr(a) if draw_alpha else None, _dev.ptr(a0), _dev.ptr(s0), _dev.ptr(s1),
+                  out_st, _dev.stream_handle(device))
+    # advance the caller's generator exactly as numpy would have
+    new_state = _pcg_jump(s, inc, int(out_st.advance)) if out_st.advance else s
+    has = int(out_st.has_uint32)
+    if out_st.advance:
+        uint = (_pcg_output(new_state) >> 32) if has else 0
+    else:
+        uint = int(st["uinteger"]) if has else 0
+    rng.bit_generator.state = {"bit_generator": "PCG64",
+                               "state": {"state": new_state, "inc": inc},
+                               "has_uint32": has, "uinteger": uint}
+    return a, a0, s0, s1
+
+
+def _uniform_ring_host(rng, count, n):
+    # fss._uniform_ring (fss.py:47-51) -- the reference's own numpy calls
+    if n == 64:
+        hi = rng.integers(0, 1 << 63, size=count, dtype=np.uint64) << np.uint64(1)
+        return hi | rng.integers(0, 2, size=count, dtype=np.uint64)
+    return rng.integers(0, 1 << n, size=count, dtype=np.uint64)
+
+
+def _sample_tape_host(n, rng, count, alpha_t, device):
+    a = alpha_t if alpha_t is not None else _dev.to_device_u64(_uniform_ring_host(rng, count, n), device)
+    a0 = _dev.to_device_u64(_uniform_ring_host(rng, count, n), device)
+    s0 = _dev.to_device_u8(prg.random_seeds(rng, count), device)
+    s1 = _dev.to_device_u8(prg.random_seeds(rng, count), device)
+    return a, a0, s0, s1
+
+
+# ---------------------------------------------------------------------------
+# Key generation (fss.py:173-340)
+# ---------------------------------------------------------------------------
+
+def _keygen_eq_core(n: int, alpha, alpha0, s0_init, s1_init):
+    """fss._keygen_eq_core (fss.py:173-216) on device (fss_dpf_keygen)."""
+    dev = alpha.device
+    count = int(alpha.shape[0])
+    alpha, alpha0 = alpha.contiguous(), alpha0.contiguous()
+    s0_init, s1_init = s0_init.contiguous(), s1_init.contiguous()
+    scw = torch.empty((n, count, 16), dtype=torch.uint8, device=dev)
+    tcw = torch.empty((n, count), dtype=torch.uint8, device=dev)
+    cw_final = torch.empty(count, dtype=torch.uint64, device=dev)
+    alpha1 = torch.empty(count, dtype=torch.uint64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.call("fss_dpf_keygen", n, count, _dev.ptr(alpha), _dev.ptr(alpha0), _dev.ptr(s0_init),
+                  _dev.ptr(s1_init), _dev.ptr(scw), _dev.ptr(tcw), _dev.ptr(cw_final),
+                  _dev.ptr(alpha1), _dev.stream_handle(dev))
+    k0 = EqKeyBatch(0, n, alpha0, s0_init, scw, tcw, cw_final)
+    k1 = EqKeyBatch(1, n, alpha1, s1_init, scw, tcw, cw_final)
+    return k0, k1
+
+
+def _keygen_cmp_core(n: int, alpha, alpha0, s0_init, s1_init, out_bits: int = None):
+    """fss._keygen_cmp_core (fss.py:219-289) on device (fss_dcf_keygen)."""
+    out_bits = n if out_bits is None else out_bits
+    dev = alpha.device
+    count = int(alpha.shape[0])
+    alpha, alpha0 = alpha.contiguous(), alpha0.contiguous()
+    s0_init, s1_init = s0_init.contiguous(), s1_init.contiguous()
+    scw = torch.empty((n, count, 16), dtype=torch.uint8, device=dev)
+    tcw = torch.empty((n, count), dtype=torch.uint8, device=dev)
+    sigma_cw = torch.empty((n, count), dtype=torch.uint64, device=dev)
+    leaf_cw = torch.empty((n + 1, count), dtype=torch.uint64, device=dev)
+    alpha1 = torch.empty(count, dtype=torch.uint64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.call("fss_dcf_keygen", n, out_bits, count, _dev.ptr(alpha), _dev.ptr(alpha0),
+                  _dev.ptr(s0_init), _dev.ptr(s1_init), _dev.ptr(scw), _dev.ptr(tcw),
+                  _dev.ptr(sigma_cw), _dev.ptr(leaf_cw), _dev.ptr(alpha1), _dev.stream_handle(dev))
+    k0 = CmpKeyBatch(0, n, alpha0, s0_init, scw, tcw, sigma_cw, leaf_cw, out_bits=out_bits)
+    k1 = CmpKeyBatch(1, n, alpha1, s1_init, scw, tcw, sigma_cw, leaf_cw, out_bits=out_bits)
+    return k0, k1
+
+
+def keygen_eq(n: int, rng: np.random.Generator, count: int = 1,
+              alpha=None, device=None):
+    """Generate ``count`` equality key pairs; returns (alpha, k0, k1) (fss.py:306-313)."""
+    if not 4 <= n <= 64:
+        raise ValueError("equality keys support 4 <= n <= 64")
+    dev = _dev.default_device(device)
+    a, a0, s0, s1 = _sample_tape(n, rng, count, alpha, dev)
+    k0, k1 = _keygen_eq_core(n, a, a0, s0, s1)
+    return a, k0, k1
+
+
+def keygen_eq_with_tape(n: int, rng: np.random.Generator, count: int = 1, device=None):
+    alpha, k0, k1 = keygen_eq(n, rng, count, device=device)
+    return alpha, k0, k1, FssTape(alpha, k0.seed0.clone(), k1.seed0.clone())
+
+
+def keygen_cmp(n: int, rng: np.random.Generator, count: int = 1,
+               alpha=None, out_bits: int = None, device=None):
+    """Generate ``count`` comparison key pairs; returns (alpha, k0, k1) (fss.py:321-335)."""
+    if not 4 <= n <= 63:
+        raise ValueError("comparison keys support 4 <= n <= 63")
+    if out_bits is not None and not n <= out_bits <= 63:
+        raise ValueError("out_bits must lie in [n, 63]")
+    dev = _dev.default_device(device)
+    a, a0, s0, s1 = _sample_tape(n, rng, count, alpha, dev)
+    k0, k1 = _keygen_cmp_core(n, a, a0, s0, s1, out_bits)
+    return a, k0, k1
+
+
+def keygen_cmp_with_tape(n: int, rng: np.random.Generator, count: int = 1, device=None):
+    alpha, k0, k1 = keygen_cmp(n, rng, count, device=device)
+    return alpha, k0, k1, FssTape(alpha, k0.seed0.clone(), k1.seed0.clone())
+
+
+# ---------------------------------------------------------------------------
+# Evaluation (fss.py:347-426)
+# ---------------------------------------------------------------------------
+
+def _broadcast_x(x, count: int, n: int, device):
+    """fss._broadcast_x (fss.py:347-354); reduction mod 2^n happens in-kernel."""
+    host = not isinstance(x, torch.Tensor)
+    if host:
+        arr = np.asarray(x, dtype=np.uint64) & ring_mask(n)
+        if arr.ndim == 0:
+            arr = np.full(count, arr, dtype=np.uint64)
+        arr = arr.reshape(-1)
+        if arr.shape[0] != count:
+            raise ValueError(f"need one public input per key: {arr.shape[0]} != {count}")
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(device)
+    else:
+        if not x.is_cuda:
+            host = "torch"  # host torch tensor (pinned for async copies): result comes back to host
+        t = _dev.to_device_u64(x, device).reshape(-1)
+        if t.numel() == 1 and count != 1:
+            t = t.expand(count).contiguous()
+        if t.shape[0] != count:
+            raise ValueError(f"need one public input per key: {t.shape[0]} != {count}")
+    return t, host
+
+
+def _result(t: torch.Tensor, host):
+    if not host:
+        return t
+    if host == "torch":
+        out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        out.copy_(t, non_blocking=True)
+        torch.cuda.current_stream(t.device).synchronize()
+        return out
+    return _dev.to_numpy(t)
+
+
+def _level_stride(k, names) -> Optional[int]:
+    """Common element stride of the level-major arrays, or None if not uniform."""
+    ld = k.scw.stride(0) // 16 if k.scw.ndim == 3 and k.scw.shape[0] else k.count
+    if k.scw.ndim == 3 and k.scw.shape[0] and (k.scw.stride(1) != 16 or k.scw.stride(2) != 1):
+        return None
+    for name in names:
+        t = getattr(k, name)
+        if t.shape[0] > 1 and (t.stride(0) != ld or t.stride(1) != 1):
+            return None
+        if t.shape[0] <= 1 and t.numel() and t.stride(-1) != 1:
+            return None
+    return max(ld, 1)
+
+
+def _eval_operands(k, names):
+    ld = _level_stride(k, names)
+    if ld is None:
+        for name in ("scw",) + tuple(names):
+            setattr(k, name, getattr(k, name).contiguous())
+        ld = max(k.count, 1)
+    return ld
+
+
+def eval_eq(party: int, k: EqKeyBatch, x):
+    """Per-party share of 1[x == alpha] (fss.py:357-377) via fss_dpf_eval."""
+    k.validate()
+    n, count, dev = k.n_bits, k.count, k.device
+    xt, host = _broadcast_x(x, count, n, dev)
+    ld = _eval_operands(k, ("tcw",))
+    seed0, cw_final = k.seed0.contiguous(), k.cw_final.contiguous()
+    out = torch.empty(count, dtype=torch.uint64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.call("fss_dpf_eval", int(party), n, count, ld, _dev.ptr(seed0), _dev.ptr(k.scw),
+                  _dev.ptr(k.tcw), _dev.ptr(cw_final), _dev.ptr(xt), _dev.ptr(out),
+                  _dev.stream_handle(dev))
+    return _result(out, host)
+
+
+def eval_cmp(party: int, k: CmpKeyBatch, x, return_levels: bool = False):
+    """Per-party share of 1[x <= alpha] (fss.py:380-426) via fss_dcf_eval.
+
+    With return_levels the per-level output terms are also returned,
+    shape (n+1, count); at most one level reconstructs to 1."""
+    k.validate()
+    n, count, dev = k.n_bits, k.count, k.device
+    xt, host = _broadcast_x(x, count, n, dev)
+    ld = _eval_operands(k, ("tcw", "sigma_cw", "leaf_cw"))
+    seed0 = k.seed0.contiguous()
+    out = torch.empty(count, dtype=torch.uint64, device=dev)
+    levels = torch.empty((n + 1, count), dtype=torch.uint64, device=dev) if return_levels else None
+    with torch.cuda.device(dev):
+        _lib.call("fss_dcf_eval", int(party), n, int(k.out_bits), count, ld, _dev.ptr(seed0),
+                  _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(k.sigma_cw), _dev.ptr(k.leaf_cw),
+                  _dev.ptr(xt), _dev.ptr(out), _dev.ptr(levels), _dev.stream_handle(dev))
+    if host:
+        out = _result(out, host)
+        levels = _result(levels, host) if return_levels else None
+    return (out, levels) if return_levels else out
+
+
+# ---------------------------------------------------------------------------
+# Masked-input protocols (fss.py:433-491)
+# ---------------------------------------------------------------------------
+
+_sign_probe = None
+
+
+def set_sign_probe(probe):
+    """Install a harness callback probe(party, y_ring, out_ring, n_bits, out_bits)
+    fired on every sign invocation (fss.py:436-441). Pass None to uninstall."""
+    global _sign_probe
+    _sign_probe = probe
+
+
+def sign_protocol(session, y, keys: CmpKeyBatch):
+    """Shares of 1[y <= 0] for an additively shared y. One online round (fss.py:444-473)."""
+    from .ring import RingTensor
+    from .sharing import AdditiveShare, mask_and_reveal
+    from . import ring_ops
+
+    m = y.values.size
+    if keys.out_bits != y.values.n_bits:
+        raise ValueError("key output ring does not match the shared input")
+    if keys.party != y.party:
+        raise ValueError("key batch belongs to the other party")
+    ks = keys.take_unused(m)
+    if keys.n_bits != y.values.n_bits:
+        # Narrow-domain keys: mask and reveal only the low domain bits.
+        y = AdditiveShare(y.party, RingTensor(ring_ops.mask(y.values.data, keys.n_bits),
+                                              keys.n_bits, _trusted=True), 0)
+    x = mask_and_reveal(session, y, ks.alpha_share.reshape(y.values.shape), op="comparison")
+    out = eval_cmp(y.party, ks, x.data.reshape(-1))
+    if _sign_probe is not None:
+        _sign_probe(y.party, y.values.data.reshape(-1), out, ks.n_bits, ks.out_bits)
+    values = RingTensor(out.reshape(y.values.shape), ks.out_bits, _trusted=True)
+    return AdditiveShare(y.party, values, precision=0)
+
+
+def eq_protocol(session, y, keys: EqKeyBatch):
+    """Shares of 1[y == 0] for an additively shared y. One online round, exact (fss.py:476-491)."""
+    from .ring import RingTensor
+    from .sharing import AdditiveShare, mask_and_reveal
+
+    m = y.values.size
+    if keys.n_bits != y.values.n_bits:
+        raise ValueError("key ring width does not match the shared input")
+    if keys.party != y.party:
+        raise ValueError("key batch belongs to the other party")
+    ks = keys.take_unused(m)
+    x = mask_and_reveal(session, y, ks.alpha_share.reshape(y.values.shape), op="equality")
+    out = eval_eq(y.party, ks, x.data.reshape(-1))
+    values = RingTensor(out.reshape(y.values.shape), y.values.n_bits, _trusted=True)
+    return AdditiveShare(y.party, values, precision=0)
+
+
+# ---------------------------------------------------------------------------
+# Serialization (container format in LAYOUT.md; fss.py:498-658)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class KeyBatch:
+    """Dealer-side transport container holding both parties' payloads."""
+
+    kind: int
+    n_bits: int
+    count: int
+    payload0: bytes
+    payload1: bytes
+
+
+def _ring_width_bytes(n: int) -> int:
+    return (n + 7) // 8
+
+
+def eq_elem_bytes(n: int) -> int:
+    """Serialized bytes per equality key element (one party), fss.py:513-516."""
+    w = _ring_width_bytes(n)
+    return w + 16 + n * 17 + w
+
+
+def cmp_elem_bytes(n: int) -> int:
+    """Serialized bytes per comparison key element (one party), fss.py:519-522."""
+    w = _ring_width_bytes(n)
+    return w + 16 + n * (17 + w) + (n + 1) * w
+
+
+def cmp_key_bits(n: int, lam: int = LAMBDA) -> int:
+    """Theoretical compressed comparison key size in bits (fss.py:525-527)."""
+    return n * (lam + 2 * n + 4) + lam + 2 * n
+
+
+def _pack_device(k) -> torch.Tensor:
+    """Element-major ARNK payload of one party as a (count, elem) device tensor."""
+    k.validate()
+    if isinstance(k, CmpKeyBatch):
+        if k.out_bits != k.n_bits:
+            raise KeyFormatError("widened-output comparison keys are in-memory only")
+        kind, elem, names = KIND_CMP, cmp_elem_bytes(k.n_bits), ("tcw", "sigma_cw", "leaf_cw")
+    else:
+        kind, elem, names = KIND_EQ, eq_elem_bytes(k.n_bits), ("tcw",)
+    dev = k.device
+    ld = _eval_operands(k, names)
+    alpha, seed0 = k.alpha_share.contiguous(), k.seed0.contiguous()
+    buf = torch.empty((k.count, elem), dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        _lib.call("fss_arnk_pack", kind, k.n_bits, k.count, ld, _dev.ptr(alpha), _dev.ptr(seed0),
+                  _dev.ptr(k.scw), _dev.ptr(k.tcw),
+                  _dev.ptr(k.cw_final.contiguous()) if kind == KIND_EQ else None,
+                  _dev.ptr(k.sigma_cw) if kind == KIND_CMP else None,
+                  _dev.ptr(k.leaf_cw) if kind == KIND_CMP else None,
+                  _dev.ptr(buf), _dev.stream_handle(dev))
+    return buf
+
+
+def _pack_eq(k: EqKeyBatch) -> bytes:
+    return _dev.to_numpy(_pack_device(k)).tobytes()
+
+
+def _pack_cmp(k: CmpKeyBatch) -> bytes:
+    if k.out_bits != k.n_bits:
+        raise KeyFormatError("widened-output comparison keys are in-memory only")
+    return _dev.to_numpy(_pack_device(k)).tobytes()
+
+
+def _unpack(kind: int, party: int, n: int, count: int, payload, device=None):
+    dev = _dev.default_device(device)
+    elem = eq_elem_bytes(n) if kind == KIND_EQ else cmp_elem_bytes(n)
+    if isinstance(payload, torch.Tensor):
+        buf = payload.to(dev).reshape(-1)
+    else:
+        buf = torch.frombuffer(bytearray(payload), dtype=torch.uint8).to(dev) if len(payload) else \
+            torch.empty(0, dtype=torch.uint8, device=dev)
+    if buf.numel() != count * elem:
+        raise KeyFormatError(f"payload size mismatch: {buf.numel()} != {count * elem}")
+    alpha = torch.empty(count, dtype=torch.uint64, device=dev)
+    seed0 = torch.empty((count, 16), dtype=torch.uint8, device=dev)
+    scw = torch.empty((n, count, 16), dtype=torch.uint8, device=dev)
+    tcw = torch.empty((n, count), dtype=torch.uint8, device=dev)
+    cw_final = sigma = leaf = None
+    if kind == KIND_EQ:
+        cw_final = torch.empty(count, dtype=torch.uint64, device=dev)
+    else:
+        sigma = torch.empty((n, count), dtype=torch.uint64, device=dev)
+        leaf = torch.empty((n + 1, count), dtype=torch.uint64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.call("fss_arnk_unpack", kind, n, count, _dev.ptr(buf), _dev.ptr(alpha),
+                  _dev.ptr(seed0), _dev.ptr(scw), _dev.ptr(tcw), _dev.ptr(cw_final),
+                  _dev.ptr(sigma), _dev.ptr(leaf), _dev.stream_handle(dev))
+    if kind == KIND_EQ:
+        return EqKeyBatch(party, n, alpha, seed0, scw, tcw, cw_final)
+    return CmpKeyBatch(party, n, alpha, seed0, scw, tcw, sigma, leaf)
+
+
+def _unpack_eq(party: int, n: int, count: int, payload, device=None) -> EqKeyBatch:
+    return _unpack(KIND_EQ, party, n, count, payload, device)
+
+
+def _unpack_cmp(party: int, n: int, count: int, payload, device=None) -> CmpKeyBatch:
+    return _unpack(KIND_CMP, party, n, count, payload, device)
+
+
+def pack_keys(k0, k1) -> KeyBatch:
+    """Bundle a key pair into the transport container (fss.py:605-613)."""
+    if type(k0) is not type(k1) or k0.n_bits != k1.n_bits or k0.count != k1.count:
+        raise ValueError("key batches do not form a pair")
+    if isinstance(k0, EqKeyBatch):
+        return KeyBatch(KIND_EQ, k0.n_bits, k0.count, _pack_eq(k0), _pack_eq(k1))
+    if isinstance(k0, CmpKeyBatch):
+        return KeyBatch(KIND_CMP, k0.n_bits, k0.count, _pack_cmp(k0), _pack_cmp(k1))
+    raise TypeError(f"cannot pack {type(k0)!r}")
+
+
+def unpack_keys(batch: KeyBatch, device=None):
+    """Rebuild the typed key pair from a container (fss.py:616-624)."""
+    if batch.kind == KIND_EQ:
+        return (_unpack_eq(0, batch.n_bits, batch.count, batch.payload0, device),
+                _unpack_eq(1, batch.n_bits, batch.count, batch.payload1, device))
+    if batch.kind == KIND_CMP:
+        return (_unpack_cmp(0, batch.n_bits, batch.count, batch.payload0, device),
+                _unpack_cmp(1, batch.n_bits, batch.count, batch.payload1, device))
+    raise KeyFormatError(f"cannot unpack kind {batch.kind}")
+
+
+def serialize_keys(batch: KeyBatch) -> bytes:
+    """ARNK header + both payloads (fss.py:627-630)."""
+    header = (MAGIC + bytes([VERSION, batch.kind, batch.n_bits])
+              + LAMBDA.to_bytes(2, "little") + batch.count.to_bytes(4, "little"))
+    return header + batch.payload0 + batch.payload1
+
+
+def deserialize_keys(data: bytes) -> KeyBatch:
+    """Parse and validate an ARNK container (fss.py:633-658)."""
+    if len(data) < _HEADER_BYTES:
+        raise KeyFormatError("truncated header")
+    if data[:4] != MAGIC:
+        raise KeyFormatError("bad magic")
+    version, kind, n = data[4], data[5], data[6]
+    if version != VERSION:
+        raise KeyFormatError(f"unsupported version {version}")
+    lam = int.from_bytes(data[7:9], "little")
+    if lam != LAMBDA:
+        raise KeyFormatError(f"unsupported lambda {lam}")
+    count = int.from_bytes(data[9:13], "little")
+    body = data[_HEADER_BYTES:]
+    if kind == KIND_EQ:
+        per = eq_elem_bytes(n) * count
+    elif kind == KIND_CMP:
+        per = cmp_elem_bytes(n) * count
+    elif kind == KIND_TRIPLE:
+        if len(body) < 4:
+            raise KeyFormatError("truncated triple payload")
+        per = int.from_bytes(body[:4], "little") + 4
+    else:
+        raise KeyFormatError(f"unknown kind {kind}")
+    if len(body) != 2 * per:
+        raise KeyFormatError(f"payload size mismatch: {len(body)} != {2 * per}")
+    return KeyBatch(kind, n, count, body[:per], body[per:])
+
+
+# ---------------------------------------------------------------------------
+# Cut-and-choose audit (fss.py:665-699)
+# ---------------------------------------------------------------------------
+
+def audit_keys(k0, k1, tape: FssTape, indices) -> list:
+    """Replay keygen from the disclosed tape on device and byte-compare the
+    packed keys with the issued ones. Returns the indices that do not match.
+    Sampled keys are marked consumed in both batches."""
+    from . import ring_ops
+
+    indices = np.asarray(list(indices) if isinstance(indices, range) else indices,
+                         dtype=np.int64).reshape(-1)
+    sub0, sub1 = k0.take(indices), k1.take(indices)
+    k0.consumed[indices] = True
+    k1.consumed[indices] = True
+    t = tape.take(indices)
+    if isinstance(k0, EqKeyBatch):
+        r0, r1 = _keygen_eq_core(k0.n_bits, t.alpha.contiguous(), sub0.alpha_share.contiguous(),
+                                 t.s0.contiguous(), t.s1.contiguous())
+    elif isinstance(k0, CmpKeyBatch):
+        if k0.out_bits != k0.n_bits:
+            raise KeyFormatError("widened-output comparison keys cannot be audited byte-wise")
+        r0, r1 = _keygen_cmp_core(k0.n_bits, t.alpha.contiguous(), sub0.alpha_share.contiguous(),
+                                  t.s0.contiguous(), t.s1.contiguous())
+    else:
+        raise TypeError(f"cannot audit {type(k0)!r}")
+    if indices.size == 0:
+        return []
+    ok = (torch.all(_pack_device(sub0) == _pack_device(r0), dim=1)
+          & torch.all(_pack_device(sub1) == _pack_device(r1), dim=1))
+    recon = ring_ops.binary("add", sub0.alpha_share.contiguous(), sub1.alpha_share.contiguous(),
+                            k0.n_bits)
+    ok &= _dev.as_i64(recon) == _dev.as_i64(t.alpha.contiguous())
+    ok = _dev.to_numpy(ok)
+    return [int(i) for i, good in zip(indices, ok) if not good]

@@ -1,0 +1,87 @@
+"""CPU-side checks: the C-ABI library loads and exports every declared symbol,
+host-side bookkeeping (PCG64 jump, index normalisation, ARNK headers)."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+
+def _declared_symbols():
+    syms = set()
+    for name in os.listdir(os.path.join(ROOT, "include")):
+        if name.endswith(".h"):
+            src = open(os.path.join(ROOT, "include", name)).read()
+            syms |= set(re.findall(r"\b(fss_[a-z0-9_]+)\s*\(", src))
+    return syms
+
+
+def test_library_exports_every_declared_symbol():
+    import ctypes
+    from paper_2006_04593_b200 import _build, _lib
+    _build.build()
+    lib = _lib.load()
+    declared = _declared_symbols()
+    assert {"fss_dcf_eval", "fss_dpf_eval", "fss_dcf_keygen", "fss_dpf_keygen",
+            "fss_aes_mmo_expand", "fss_pcg64_tape", "fss_arnk_pack"} <= declared
+    for sym in declared:
+        assert hasattr(lib, sym), sym
+    assert set(_lib.SIGNATURES) >= declared
+    assert lib.fss_abi_version() == 1
+    assert lib.fss_arnk_elem_bytes(1, 32) == 824 and lib.fss_arnk_elem_bytes(0, 32) == 568
+    assert isinstance(ctypes.CDLL(_build.LIB), ctypes.CDLL)
+
+
+def test_library_rejects_bad_arguments_without_gpu():
+    from paper_2006_04593_b200 import _lib
+    lib = _lib.load()
+    assert lib.fss_dcf_eval(2, 32, 32, 1, 1, None, None, None, None, None, None, None, None, None) == 1
+    assert b"party" in lib.fss_last_error()
+    assert lib.fss_aes_mmo_expand(None, 1, 4, None, None) == 1
+    with pytest.raises(ValueError):
+        _lib.check(1, "x")
+
+
+def test_pcg_jump_matches_numpy():
+    from paper_2006_04593_b200.fss import _pcg_jump, _pcg_output
+    rng = np.random.default_rng(99)
+    st = rng.bit_generator.state["state"]
+    for delta in (1, 2, 5, 1000, 123456789):
+        r = np.random.default_rng(99)
+        r.bit_generator.advance(delta - 1)
+        want = r.bit_generator.random_raw()
+        s = _pcg_jump(st["state"], st["inc"], delta)
+        assert _pcg_output(s) == int(want)
+
+
+def test_index_normalisation():
+    from paper_2006_04593_b200.fss import _index
+    sel, arr = _index(np.arange(3, 9), 10, None)
+    assert sel == slice(3, 9) and list(arr) == list(range(3, 9))
+    sel, arr = _index([-1], 10, None)
+    assert sel == slice(9, 10)
+    sel, arr = _index(range(2, 4), 10, None)
+    assert sel == slice(2, 4)
+    with pytest.raises(IndexError):
+        _index([10], 10, None)
+
+
+def test_deserialize_header_errors():
+    from paper_2006_04593_b200 import fss
+    blob = fss.serialize_keys(fss.KeyBatch(fss.KIND_EQ, 8, 0, b"", b""))
+    assert len(blob) == 13 and fss.deserialize_keys(blob).count == 0
+    with pytest.raises(fss.KeyFormatError, match="bad magic"):
+        fss.deserialize_keys(b"XXXX" + blob[4:])
+    with pytest.raises(fss.KeyFormatError, match="version"):
+        fss.deserialize_keys(blob[:4] + bytes([9]) + blob[5:])
+    with pytest.raises(fss.KeyFormatError, match="truncated"):
+        fss.deserialize_keys(blob[:5])
+    one = fss.serialize_keys(fss.KeyBatch(fss.KIND_CMP, 16, 1, bytes(fss.cmp_elem_bytes(16)),
+                                          bytes(fss.cmp_elem_bytes(16))))
+    with pytest.raises(fss.KeyFormatError, match="size mismatch"):
+        fss.deserialize_keys(one[:-3])
+    assert fss.cmp_key_bits(32) == 6431 and fss.cmp_elem_bytes(32) == 824
+    assert fss.eq_elem_bytes(32) == 568
