@@ -41,7 +41,7 @@ def random_seeds(rng: np.random.Generator, count: int) -> np.ndarray:
 def _seeds_in(seeds):
     host = not isinstance(seeds, torch.Tensor)
     if host:
-        arr = np.ascontiguousarray(seeds, dtype=np.uint8)
+        arr = np.array(seeds, dtype=np.uint8, copy=True, order="C")
         if arr.ndim != 2 or arr.shape[1] != BLOCK_BYTES:
             raise ValueError("seeds must have shape (N, 16)")
         dev = _dev.default_device()
@@ -71,7 +71,7 @@ def expand_one(seed: bytes, out_blocks: int) -> bytes:
     """Single-seed convenience wrapper (prg.py:63-68)."""
     if len(seed) != BLOCK_BYTES:
         raise ValueError("seed must be 16 bytes")
-    arr = np.frombuffer(seed, dtype=np.uint8).reshape(1, BLOCK_BYTES)
+    arr = np.frombuffer(seed, dtype=np.uint8).reshape(1, BLOCK_BYTES).copy()
     return expand(arr, out_blocks).tobytes()
 
 
