@@ -41,7 +41,9 @@ N_BITS = 32
 BYTES_PER_EVAL = 16 + 32 * 16 + 32 + 32 * 8 + 33 * 8 + 8 + 8   # 1096 B
 AES_PER_EVAL = 64                                              # 32 levels x 2 blocks
 LDS_PER_AES = 160                                              # T-table lookups per block
-LDS_PER_CLK_SM = 32                                            # 128 B/clk smem crossbar
+WAVEFRONTS_PER_AES = LDS_PER_AES / 32                          # one conflict-free LDS.32 wavefront
+                                                               # serves 32 lanes' lookups
+LOP3_PER_AES_BITSLICED = 356.25                                # SURVEY.md §8d bitsliced floor
 
 
 def _args():
@@ -54,6 +56,7 @@ def _args():
     p.add_argument("--cpu-log2n", type=int, default=20, help="CPU sample size (reference arm)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-secondary", action="store_true")
     return p.parse_args()
 
 
@@ -177,7 +180,7 @@ def cpu_baseline_line(log2n: int):
     x = alpha.copy()
     oracle.eval_cmp(0, k0, x)
     reps, t_total = 0, 0.0
-    while t_total < 5.0 and reps < 20:
+    while t_total < 10.0 and reps < 100:
         t0 = time.perf_counter()
         oracle.eval_cmp(0, k0, x)
         oracle.eval_cmp(1, k1, x)
@@ -197,6 +200,50 @@ def load_traffic():
         return d.get("dram_bytes_per_party_eval")
     except (OSError, ValueError):
         return None
+
+
+def measure_secondary(dev, args):
+    """Keygen and DPF numbers beside the headline (keygen and eval timed
+    separately): CUDA events on the launching stream, 2^22
+    elements, best of 3 after one warm-up."""
+    import numpy as np
+    import torch
+
+    from paper_2006_04593_b200 import fss
+
+    N = 1 << min(22, args.log2n)
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(fn):
+        fn()
+        best = None
+        for _ in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            b.synchronize()
+            t = a.elapsed_time(b) / 1e3
+            best = t if best is None else min(best, t)
+        return best
+
+    out = {"elements": N}
+    rng = np.random.default_rng(77)
+    t = timed(lambda: fss.keygen_cmp(N_BITS, rng, N, device=dev))
+    out["dcf_keygen_pairs_per_s"] = N / t
+    out["dcf_keygen_aes_per_s"] = N * 192 / t
+    t = timed(lambda: fss.keygen_eq(N_BITS, rng, N, device=dev))
+    out["dpf_keygen_pairs_per_s"] = N / t
+    alpha, e0, e1 = fss.keygen_eq(N_BITS, rng, N, device=dev)
+    x = alpha.clone()
+    t = timed(lambda: fss.eval_eq(0, e0, x))
+    out["dpf_eval_party_evals_per_s"] = N / t
+    out["dpf_eval_aes_per_s"] = N * 32 / t
+    rec = (fss.eval_eq(0, e0, x).view(torch.int64) + fss.eval_eq(1, e1, x).view(torch.int64)) & 0xFFFFFFFF
+    assert bool((rec == 1).all()), "DPF reconstruction mismatch"
+    del alpha, e0, e1, x, rec
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_ours(args, ws, rank, local):
@@ -272,51 +319,75 @@ def run_ours(args, ws, rank, local):
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
     aes_rate = N * AES_PER_EVAL / avg_launch_s
-    aes_peak = sms * sm_max * 1e6 * LDS_PER_CLK_SM / LDS_PER_AES
+    peaks_live = _lib.probe_peaks()   # measured on this box, this run
+    lds_peak_aes = peaks_live["lds_wavefronts_per_s"] / WAVEFRONTS_PER_AES
+    alu_peak_aes = peaks_live["lop3_lane_ops_per_s"] / LOP3_PER_AES_BITSLICED
+    secondary = measure_secondary(dev, args) if not args.no_secondary else None
     del out0, out1, rec
 
     # ---- e2e through the public API with host buffers ----------------------
     e2e = None
     if not args.no_e2e:
-        del k0, k1, alpha, x, y
-        torch.cuda.empty_cache()
         x_host = torch.empty(N, dtype=torch.int64, pin_memory=True)
         x_host.copy_(torch.from_numpy(np.random.default_rng(5 + rank).integers(
             0, 1 << 32, N, dtype=np.uint64).view(np.int64)))
         x_host = x_host.view(torch.uint64)
-        rng2 = np.random.default_rng(2000 + rank)
 
+        def timed_host(step, steps):
+            barrier()
+            torch.cuda.synchronize()
+            e_start = torch.cuda.Event(enable_timing=True)
+            e_end = torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e_start.record(stream)
+            for _ in range(steps):
+                step()
+            e_end.record(stream)
+            torch.cuda.synchronize()
+            wall = time.perf_counter() - t0
+            return max_over_ranks(max(e_start.elapsed_time(e_end) / 1e3, wall))
+
+        # (1) online comparison through the public API: keys resident in HBM
+        # (dealt before, like the reference arm's keys), pinned host x in,
+        # pinned host shares out -- every step copies x up and both shares down.
         def e2e_step():
-            a, q0, q1 = fss.keygen_cmp(N_BITS, rng2, N, device=dev)
-            r0 = fss.eval_cmp(0, q0, x_host)      # pinned host in -> pinned host out
-            r1 = fss.eval_cmp(1, q1, x_host)
+            r0 = fss.eval_cmp(0, k0, x_host)      # pinned host in -> pinned host out
+            r1 = fss.eval_cmp(1, k1, x_host)
             return r0, r1
 
         for _ in range(args.warmup):
             r0, r1 = e2e_step()
-        barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        e_start = torch.cuda.Event(enable_timing=True)
-        e_end = torch.cuda.Event(enable_timing=True)
-        e_start.record(stream)
-        for _ in range(args.steps):
-            r0, r1 = e2e_step()
-        e_end.record(stream)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
-        t_e2e = max_over_ranks(max(e_start.elapsed_time(e_end) / 1e3, wall))
+        want = (x_host.view(torch.int64) <= alpha.view(torch.int64).cpu()).to(torch.int64)
+        assert torch.equal((r0.view(torch.int64) + r1.view(torch.int64)) & 0xFFFFFFFF, want)
+        t_e2e = timed_host(e2e_step, args.steps)
         e2e = {"value": ws * N * args.steps / t_e2e, "unit": "comparisons/s",
-               "h2d_bytes_per_step": 2 * N * 8 + 48,
-               "d2h_bytes_per_step": 2 * N * 8,
-               "step": "keygen_cmp(32, numpy Generator, 2^%d) + eval_cmp(party 0/1, pinned host x) "
+               "h2d_bytes_per_step": 2 * N * 8, "d2h_bytes_per_step": 2 * N * 8,
+               "step": "fss.eval_cmp(party 0 and 1, HBM-resident keys, pinned host x of 2^%d u64) "
                        "-> pinned host shares" % args.log2n}
+        del k0, k1, alpha, x, y
+        torch.cuda.empty_cache()
+
+        # (2) dealer + online: keygen_cmp from the host numpy Generator (tape
+        # drawn on device from its PCG64 state) inside every step as well.
+        rng2 = np.random.default_rng(2000 + rank)
+
+        def e2e_keygen_step():
+            _, q0, q1 = fss.keygen_cmp(N_BITS, rng2, N, device=dev)
+            return fss.eval_cmp(0, q0, x_host), fss.eval_cmp(1, q1, x_host)
+
+        e2e_keygen_step()
+        ksteps = max(3, args.steps // 4)
+        t_kg = timed_host(e2e_keygen_step, ksteps)
+        e2e["with_keygen"] = {"value": ws * N * ksteps / t_kg, "unit": "comparisons/s",
+                              "steps": ksteps,
+                              "step": "keygen_cmp(32, numpy Generator, 2^%d) + the eval step above"
+                                      % args.log2n}
 
     if rank != 0:
         if ws > 1:
             dist.destroy_process_group()
         return
-    cpu = None if (args.no_cpu or ws > 1) else cpu_baseline_line(16)
+    cpu = None if (args.no_cpu or ws > 1) else cpu_baseline_line(args.cpu_log2n)
     line = {
         "metric": "FSS comparisons/sec (DCF eval, n=32)",
         "value": value, "unit": "comparisons/s", "n_gpus": ws, "steps": args.steps,
@@ -326,15 +397,27 @@ def run_ours(args, ws, rank, local):
                                "both parties per step, keys resident in HBM",
                    "global_batch": ws * N, "seq_len": None, "parallelism": f"dp{ws} (element shards)",
                    "l2": "inputs larger than L2 (18 GB of keys per GPU)"},
-        "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved_gbs / hbm_peak,
+        "roofline": {"bound": "smem-lookup", "achieved": aes_rate, "peak": lds_peak_aes,
+                     "unit": "AES-blocks/s", "frac": aes_rate / lds_peak_aes,
                      "traffic": (traffic * N if traffic else None),
-                     "note": "kernel dcf_eval_kernel; 1096 algorithmic B per party-eval; the "
-                             "binding roof is compute_roofline (shared-memory T-table lookups)"},
-        "compute_roofline": {"bound": "smem-lookup", "achieved": aes_rate, "peak": aes_peak,
-                             "unit": "AES-blocks/s", "frac": aes_rate / aes_peak,
-                             "note": f"{AES_PER_EVAL} AES/party-eval, {LDS_PER_AES} LDS/AES, "
-                                     f"{LDS_PER_CLK_SM} LDS/clk/SM x {sms} SMs x {sm_max:.0f} MHz"},
+                     "kernel": "dcf_eval_kernel",
+                     "note": (f"{AES_PER_EVAL} AES blocks per party-eval x 2^{args.log2n} party-evals "
+                              "per launch / CUDA-event launch time; peak = measured conflict-free "
+                              f"LDS wavefront rate on this GPU ({peaks_live['lds_wavefronts_per_s']:.4g}/s, "
+                              f"fss_probe_peaks) / {WAVEFRONTS_PER_AES:g} wavefronts per AES block "
+                              "(160 T-table lookups); traffic = ncu DRAM bytes per launch "
+                              "(profiles/ncu_dcf_eval.json x N)")},
+        "alu_roofline": {"bound": "alu", "achieved": aes_rate, "peak": alu_peak_aes,
+                         "unit": "AES-blocks/s", "frac": aes_rate / alu_peak_aes,
+                         "note": (f"bitsliced-AES ALU roof of SURVEY.md 8d: measured LOP3 rate "
+                                  f"{peaks_live['lop3_lane_ops_per_s']:.4g} lane-ops/s / "
+                                  f"{LOP3_PER_AES_BITSLICED} LOP3 per block")},
+        "hbm_roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved_gbs / hbm_peak,
+                         "note": f"{BYTES_PER_EVAL} algorithmic B per party-eval; peak = "
+                                 "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+        "peaks_probe": peaks_live,
+        "secondary": secondary,
         "kernel_ms_per_launch": avg_launch_s * 1e3,
         "clocks": clocks,
         "gpu_launches": 2 * args.steps,

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define FSS_ABI_VERSION 1
+#define FSS_ABI_VERSION 2
 #define FSS_OK 0
 #define FSS_EINVAL 1
 #define FSS_ECUDA 2
@@ -106,12 +106,40 @@ int fss_arnk_unpack(int kind, int n, uint64_t count, const uint8_t* payload, uin
 int fss_ring_op(int op, int n_bits, uint64_t count, const uint64_t* a, const uint64_t* b,
                 uint64_t b_scalar, uint64_t* out, void* stream);
 
-/* Elementwise Beaver product share (beaver.py:257-294 with OP_MUL): delta/eps are
- * opened from own+peer masked shares, z = delta*b + a*eps + c (+ delta*eps, party 0). */
-int fss_beaver_mul(int party, int n_bits, uint64_t count, const uint64_t* delta_own,
-                   const uint64_t* delta_peer, const uint64_t* eps_own, const uint64_t* eps_peer,
+/* Wire format (sharing.py:191-207): ring values travel at the smallest
+ * power-of-two width covering n_bits -- 1, 2, 4 or 8 bytes, little-endian. */
+int fss_wire_bytes(int n_bits);
+
+/* wire[i] = (a[i] op b[i]) mod 2^n_bits at wire width; op FSS_RING_ADD or
+ * FSS_RING_SUB; b == NULL packs a alone. mask_and_reveal's m_j = y_j + alpha_j
+ * (sharing.py:224-226), reveal's own share (sharing.py:233-242), Beaver's
+ * delta_j = x_j - a_j / eps_j = y_j - b_j (beaver.py:279-281). */
+int fss_wire_pack(int op, int n_bits, uint64_t count, const uint64_t* a, const uint64_t* b,
+                  void* wire, void* stream);
+
+/* out[i] = (own[i] + peer[i]) mod 2^n_bits from two wire buffers (peer may be
+ * NULL): the public x = m_0 + m_1 both parties reconstruct (sharing.py:228-230). */
+int fss_wire_open(int n_bits, uint64_t count, const void* own, const void* peer, uint64_t* out,
+                  void* stream);
+
+/* Elementwise Beaver product share (beaver.py:257-294 with OP_MUL), fused with
+ * the opening: delta = d_own + d_peer, eps = e_own + e_peer (wire width),
+ * z = delta*b + a*eps + c (+ delta*eps, party 0). */
+int fss_beaver_mul(int party, int n_bits, uint64_t count, const void* delta_own,
+                   const void* delta_peer, const void* eps_own, const void* eps_peer,
                    const uint64_t* a, const uint64_t* b, const uint64_t* c, uint64_t* z,
                    void* stream);
+
+/* Diagnostics (not a reference entry point): on-box peak probes used as the
+ * roofline denominators of the AES work. Synchronous; runs ~10 ms of probe
+ * kernels on the current device. */
+typedef struct {
+    double lds_wavefronts_per_s;  /* conflict-free LDS.32 warp lookups, T-table access pattern */
+    double lop3_lane_ops_per_s;   /* lop3.b32 lane-ops */
+    double sm_clock_hz;           /* SM clock seen by the LDS probe (clock64 / globaltimer) */
+    int32_t sms;
+} fss_peaks;
+int fss_probe_peaks(fss_peaks* out);
 
 #ifdef __cplusplus
 }

@@ -27,6 +27,11 @@ class PcgState(ctypes.Structure):
                 ("advance", ctypes.c_uint64)]
 
 
+class Peaks(ctypes.Structure):
+    _fields_ = [("lds_wavefronts_per_s", ctypes.c_double), ("lop3_lane_ops_per_s", ctypes.c_double),
+                ("sm_clock_hz", ctypes.c_double), ("sms", ctypes.c_int32)]
+
+
 # name -> argtypes (all return int status unless listed in _RESTYPE)
 SIGNATURES = {
     "fss_abi_version": [],
@@ -43,6 +48,10 @@ SIGNATURES = {
     "fss_arnk_unpack": [_int, _int, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "fss_ring_op": [_int, _int, _u64, _vp, _vp, _u64, _vp, _vp],
     "fss_beaver_mul": [_int, _int, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "fss_wire_bytes": [_int],
+    "fss_wire_pack": [_int, _int, _u64, _vp, _vp, _vp, _vp],
+    "fss_wire_open": [_int, _u64, _vp, _vp, _vp, _vp],
+    "fss_probe_peaks": [ctypes.POINTER(Peaks)],
 }
 _RESTYPE = {"fss_last_error": ctypes.c_char_p, "fss_arnk_elem_bytes": ctypes.c_uint64}
 
@@ -81,3 +90,12 @@ def check(rc: int, what: str):
 
 def call(name: str, *args):
     check(getattr(load(), name)(*args), name)
+
+
+def probe_peaks() -> dict:
+    """Measured integer-pipe peaks of the current device (fss_probe_peaks)."""
+    p = Peaks()
+    call("fss_probe_peaks", ctypes.byref(p))
+    return {"lds_wavefronts_per_s": p.lds_wavefronts_per_s,
+            "lop3_lane_ops_per_s": p.lop3_lane_ops_per_s,
+            "sm_clock_hz": p.sm_clock_hz, "sms": p.sms}

@@ -1,5 +1,6 @@
-// Elementwise Z_2^n ring arithmetic for the share layer (reference ring.py:99-129,
-// sharing.py:214-230 mask_and_reveal, beaver.py:257-294 Beaver combine).
+// Elementwise Z_2^n ring arithmetic for the share layer (reference ring.py:99-129),
+// the wire packing of the one masked message (sharing.py:191-230) and the
+// Beaver combine (beaver.py:257-294).
 // u64 words, wraparound mod 2^64 then mask (ring.py:107-114). Vectorised:
 // each thread handles two u64 (one 16-byte load per operand).
 #include <cuda_runtime.h>
@@ -29,18 +30,65 @@ __global__ void ring_kernel(int op, uint64_t mask, uint64_t count, const uint64_
     }
 }
 
-// Beaver elementwise combine (beaver.py:286-292):
+// Wire format of the share layer (sharing.py:191-207 pack_ring/_wire_dtype):
+// ring values travel at the smallest power-of-two byte width covering n_bits.
+template <typename W>
+__device__ __forceinline__ uint64_t wire_ld(const void* p, uint64_t i) {
+    return (uint64_t)reinterpret_cast<const W*>(p)[i];
+}
+
+__device__ __forceinline__ uint64_t wire_get(int wb, const void* p, uint64_t i) {
+    switch (wb) {
+        case 1: return wire_ld<uint8_t>(p, i);
+        case 2: return wire_ld<uint16_t>(p, i);
+        case 4: return wire_ld<uint32_t>(p, i);
+        default: return wire_ld<uint64_t>(p, i);
+    }
+}
+
+__device__ __forceinline__ void wire_put(int wb, void* p, uint64_t i, uint64_t v) {
+    switch (wb) {
+        case 1: reinterpret_cast<uint8_t*>(p)[i] = (uint8_t)v; break;
+        case 2: reinterpret_cast<uint16_t*>(p)[i] = (uint16_t)v; break;
+        case 4: reinterpret_cast<uint32_t*>(p)[i] = (uint32_t)v; break;
+        default: reinterpret_cast<uint64_t*>(p)[i] = v;
+    }
+}
+
+// wire = (a op b) & mask  (mask_and_reveal's y + alpha, Beaver's x - a / y - b)
+__global__ void wire_pack_kernel(int op, int wb, uint64_t mask, uint64_t count,
+                                 const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
+                                 void* __restrict__ wire) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
+        const uint64_t bv = b ? b[i] : 0;
+        wire_put(wb, wire, i, apply(op, a[i], bv) & mask);
+    }
+}
+
+// out = (own + peer) & mask: the public value both parties reconstruct
+__global__ void wire_open_kernel(int wb, uint64_t mask, uint64_t count, const void* __restrict__ own,
+                                 const void* __restrict__ peer, uint64_t* __restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
+        const uint64_t p = peer ? wire_get(wb, peer, i) : 0;
+        out[i] = (wire_get(wb, own, i) + p) & mask;
+    }
+}
+
+// Beaver elementwise combine (beaver.py:281-292) fused with the opening of
+// delta and eps from the two parties' wire messages:
 //   delta = d_own + d_peer, eps = e_own + e_peer,
 //   z = delta*b + a*eps + c (+ delta*eps for party 0)
-__global__ void beaver_kernel(int party, uint64_t mask, uint64_t count,
-                              const uint64_t* __restrict__ d_own, const uint64_t* __restrict__ d_peer,
-                              const uint64_t* __restrict__ e_own, const uint64_t* __restrict__ e_peer,
+__global__ void beaver_kernel(int party, int wb, uint64_t mask, uint64_t count,
+                              const void* __restrict__ d_own, const void* __restrict__ d_peer,
+                              const void* __restrict__ e_own, const void* __restrict__ e_peer,
                               const uint64_t* __restrict__ ta, const uint64_t* __restrict__ tb,
                               const uint64_t* __restrict__ tc, uint64_t* __restrict__ z) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += stride) {
-        const uint64_t d = (d_own[i] + d_peer[i]) & mask;
-        const uint64_t e = (e_own[i] + e_peer[i]) & mask;
+        const uint64_t d = (wire_get(wb, d_own, i) + wire_get(wb, d_peer, i)) & mask;
+        const uint64_t e = (wire_get(wb, e_own, i) + wire_get(wb, e_peer, i)) & mask;
         uint64_t v = d * tb[i] + ta[i] * e + tc[i];
         if (party == 0) v += d * e;
         z[i] = v & mask;
@@ -79,8 +127,35 @@ int fss_ring_op(int op, int n_bits, uint64_t count, const uint64_t* a, const uin
     return done();
 }
 
-int fss_beaver_mul(int party, int n_bits, uint64_t count, const uint64_t* delta_own,
-                   const uint64_t* delta_peer, const uint64_t* eps_own, const uint64_t* eps_peer,
+int fss_wire_bytes(int n_bits) {
+    if (n_bits < 1 || n_bits > 64) return 0;
+    return n_bits <= 8 ? 1 : n_bits <= 16 ? 2 : n_bits <= 32 ? 4 : 8;
+}
+
+int fss_wire_pack(int op, int n_bits, uint64_t count, const uint64_t* a, const uint64_t* b,
+                  void* wire, void* stream) {
+    if (n_bits < 1 || n_bits > 64) return fssb::set_error(FSS_EINVAL, "ring width out of range");
+    if (op != FSS_RING_ADD && op != FSS_RING_SUB)
+        return fssb::set_error(FSS_EINVAL, "wire pack supports add/sub only");
+    if (count == 0) return FSS_OK;
+    const uint64_t mask = n_bits >= 64 ? ~0ULL : ((1ULL << n_bits) - 1);
+    wire_pack_kernel<<<grid_size(count), 256, 0, (cudaStream_t)stream>>>(
+        op, fss_wire_bytes(n_bits), mask, count, a, b, wire);
+    return done();
+}
+
+int fss_wire_open(int n_bits, uint64_t count, const void* own, const void* peer, uint64_t* out,
+                  void* stream) {
+    if (n_bits < 1 || n_bits > 64) return fssb::set_error(FSS_EINVAL, "ring width out of range");
+    if (count == 0) return FSS_OK;
+    const uint64_t mask = n_bits >= 64 ? ~0ULL : ((1ULL << n_bits) - 1);
+    wire_open_kernel<<<grid_size(count), 256, 0, (cudaStream_t)stream>>>(
+        fss_wire_bytes(n_bits), mask, count, own, peer, out);
+    return done();
+}
+
+int fss_beaver_mul(int party, int n_bits, uint64_t count, const void* delta_own,
+                   const void* delta_peer, const void* eps_own, const void* eps_peer,
                    const uint64_t* a, const uint64_t* b, const uint64_t* c, uint64_t* z,
                    void* stream) {
     if (party != 0 && party != 1) return fssb::set_error(FSS_EINVAL, "party must be 0 or 1");
@@ -88,7 +163,8 @@ int fss_beaver_mul(int party, int n_bits, uint64_t count, const uint64_t* delta_
     if (count == 0) return FSS_OK;
     const uint64_t mask = n_bits >= 64 ? ~0ULL : ((1ULL << n_bits) - 1);
     beaver_kernel<<<grid_size(count), 256, 0, (cudaStream_t)stream>>>(
-        party, mask, count, delta_own, delta_peer, eps_own, eps_peer, a, b, c, z);
+        party, fss_wire_bytes(n_bits), mask, count, delta_own, delta_peer, eps_own, eps_peer, a, b,
+        c, z);
     return done();
 }
 

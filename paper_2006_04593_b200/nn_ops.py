@@ -1,0 +1,143 @@
+"""Drop-in for the FSS-backed layers of the reference's ``ariann.nn_ops``
+(pkg/src/ariann/nn_ops.py:83-190): private ReLU, argmax and MaxPool built from
+the sign / equality protocols (DCF / DPF evaluation kernels) and the
+elementwise Beaver product.
+
+Round budgets are the reference's: comparison 1, ReLU 2, argmax 2, maxpool 3,
+maxpool_k2 4. Every step runs on device: the masked messages are wire-packed
+kernels, evaluation is ``fss_dcf_eval`` / ``fss_dpf_eval`` and the products are
+``fss_beaver_mul``; window extraction and the small reductions are device
+tensor ops.
+
+Beyond the reference: ``maxpool`` and ``maxpool_k2``
+also accept a batch of planes (..., m, m) and pool all of them in the same 3 /
+4 rounds (the reference's ``unroll`` takes a single 2-D plane,
+beaver.py:171-172). The batched form draws one key batch for all planes
+(``PartyPrep.maxpool(m, k, stride, planes=P)``); with P = 1 it is exactly the
+reference's call sequence.
+
+Out of scope here: ``break_ties`` and the BatchNorm / Newton protocols
+(nn_ops.py:126-266), which are not on the FSS evaluation path.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _dev, fss
+from .beaver import BeaverTriple, mul_protocol, unroll_planes
+from .ring import RingTensor
+from .sharing import AdditiveShare
+
+
+@dataclass
+class ReluPrep:
+    cmp: fss.CmpKeyBatch
+    triple: BeaverTriple
+
+
+@dataclass
+class ArgmaxPrep:
+    cmp: fss.CmpKeyBatch
+    eq: fss.EqKeyBatch
+
+
+@dataclass
+class MaxpoolPrep:
+    argmax: ArgmaxPrep
+    dot_triple: BeaverTriple
+
+
+@dataclass
+class MaxpoolK2Prep:
+    level1: ReluPrep
+    level2: ReluPrep
+
+
+def relu(session, x: AdditiveShare, prep: ReluPrep) -> AdditiveShare:
+    """max(x, 0) elementwise; exactly 0 at x == 0. Two rounds (nn_ops.py:83-94).
+
+    Sign test on x + 1, b = 1 - 1[x <= -1] = 1[x >= 0], then one product b * x."""
+    shifted = AdditiveShare(x.party, x.values, 0).add_public(1)
+    s = fss.sign_protocol(session, shifted, prep.cmp)
+    b = (-s).add_public(1)
+    return mul_protocol(session, b, AdditiveShare(x.party, x.values, x.precision), prep.triple)
+
+
+def relu_mask(session, x: AdditiveShare, cmp_keys: fss.CmpKeyBatch) -> AdditiveShare:
+    """Shares of 1[x >= 0] only, one round (nn_ops.py:97-101)."""
+    shifted = AdditiveShare(x.party, x.values, 0).add_public(1)
+    s = fss.sign_protocol(session, shifted, cmp_keys)
+    return (-s).add_public(1)
+
+
+def _pairwise_diffs(data: torch.Tensor, m: int) -> torch.Tensor:
+    """[..., j, i] = x_i - x_j with the diagonal removed, grouped by j
+    (nn_ops.py:111-114): (..., m*(m-1))."""
+    v = _dev.as_i64(data)
+    diffs = v[..., None, :] - v[..., :, None]
+    off = ~torch.eye(m, dtype=torch.bool, device=v.device)
+    return _dev.as_u64(diffs[..., off])
+
+
+def argmax(session, x: AdditiveShare, prep: ArgmaxPrep) -> AdditiveShare:
+    """Maximum indicator over the last axis; two rounds (nn_ops.py:104-123)."""
+    m = x.shape[-1]
+    if m < 2:
+        raise ValueError("argmax needs at least two entries")
+    y = AdditiveShare(x.party, RingTensor(_pairwise_diffs(x.values.data, m), x.n_bits), 0)
+    s = fss.sign_protocol(session, y, prep.cmp)  # 1[x_i <= x_j]
+    counts = s.reshape(*s.shape[:-1], m, m - 1).sum(axis=-1)
+    centered = counts.add_public(-(m - 1))
+    return fss.eq_protocol(session, centered, prep.eq)
+
+
+def _windows(x: AdditiveShare, k: int, stride: int):
+    if x.values.data.ndim < 2 or x.shape[-1] != x.shape[-2]:
+        raise ValueError("maxpool expects square planes (..., m, m)")
+    m = x.shape[-1]
+    if k > m:
+        raise ValueError(f"kernel {k} larger than input {m}")
+    win = unroll_planes(x.values.data, k, stride)             # (..., W, k*k)
+    lead = tuple(x.shape[:-2])
+    return win, lead, (m - k) // stride + 1
+
+
+def maxpool(session, x: AdditiveShare, k: int, prep: MaxpoolPrep, stride: int = 2) -> AdditiveShare:
+    """Max pooling over k x k windows of m x m planes; three rounds (nn_ops.py:157-176).
+
+    The argmax input is scaled by k^2 and biased by the in-window index so the
+    indicator stays one-hot under ties."""
+    win, lead, side = _windows(x, k, stride)
+    kk = k * k
+    flat = win.reshape(-1, kk)
+    wshare = AdditiveShare(x.party, RingTensor(flat, x.n_bits, _trusted=True), x.precision)
+    bias = torch.arange(kk, device=flat.device, dtype=torch.int64).expand(flat.shape[0], kk)
+    perturbed = wshare.mul_public_int(kk).add_public(
+        RingTensor(_dev.as_u64(bias.contiguous()), x.n_bits, _trusted=True))
+    onehot = argmax(session, perturbed, prep.argmax)
+    prods = mul_protocol(session, onehot, wshare, prep.dot_triple)
+    pooled = prods.sum(axis=-1)
+    return pooled.reshape(*lead, side, side)
+
+
+def maxpool_k2(session, x: AdditiveShare, prep: MaxpoolK2Prep) -> AdditiveShare:
+    """k=2 max pooling as a two-level max tree, max(a, b) = b + ReLU(a - b);
+    four rounds (nn_ops.py:179-190)."""
+    win, lead, side = _windows(x, 2, 2)
+    flat = win.reshape(-1, 4)
+    w = AdditiveShare(x.party, RingTensor(flat, x.n_bits, _trusted=True), x.precision)
+    lhs = AdditiveShare(x.party, RingTensor(flat[:, [0, 2]].contiguous(), x.n_bits, _trusted=True),
+                        x.precision)
+    rhs = AdditiveShare(x.party, RingTensor(flat[:, [1, 3]].contiguous(), x.n_bits, _trusted=True),
+                        x.precision)
+    del w
+    mx = rhs + relu(session, lhs - rhs, prep.level1)
+    a = AdditiveShare(x.party, RingTensor(mx.values.data[:, 0].contiguous(), x.n_bits,
+                                          _trusted=True), x.precision)
+    b = AdditiveShare(x.party, RingTensor(mx.values.data[:, 1].contiguous(), x.n_bits,
+                                          _trusted=True), x.precision)
+    out = b + relu(session, a - b, prep.level2)
+    return out.reshape(*lead, side, side)

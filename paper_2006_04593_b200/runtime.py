@@ -1,0 +1,329 @@
+"""Drop-in for the reference's ``ariann.runtime`` (pkg/src/ariann/runtime.py):
+sessions, framed exchanges and round accounting -- with device-resident
+payloads.
+
+The reference moves ``bytes`` frames over queues or TCP (runtime.py:50-210).
+Here a payload is a device tensor (the wire-packed ring values produced by the
+share layer's kernels) and the transports move it without leaving HBM:
+
+* ``LocalTransport`` -- both parties in one process (one thread each, as
+  ``run_local_pair`` in runtime.py:285-311). A send hands the tensor itself to
+  the peer together with a CUDA event recorded on the sender's stream; the
+  receiver's stream waits on that event, so the exchange is a stream-ordered
+  device-to-device hand-off (zero copies, no host round trip).
+* ``DistTransport`` -- one party per process (rank), over ``torch.distributed``
+  point-to-point (NCCL over NVLink / NVSwitch on GPUs, gloo on CPU for tests).
+  A 3-word header (tag, dtype code, numel) precedes each payload so frame
+  desync and size errors are detected like the reference's frame checks
+  (runtime.py:246-255).
+
+Round semantics are the reference's: one ``exchange`` = one matched send and
+receive = one round recorded in the ``RoundLedger`` with the payload bytes.
+"""
+
+from __future__ import annotations
+
+import os
+import queue
+import threading
+from dataclasses import dataclass, field
+
+import torch
+
+FRAME_REVEAL = 0x01
+FRAME_MASKED = 0x02
+FRAME_TRIPLE_DELTA = 0x03
+FRAME_CONTROL = 0x04
+FRAME_ABORT = 0x05
+
+_FRAME_TAGS = {FRAME_REVEAL, FRAME_MASKED, FRAME_TRIPLE_DELTA, FRAME_CONTROL, FRAME_ABORT}
+
+DEFAULT_TIMEOUT_MS = 30_000
+
+
+def timeout_seconds() -> float:
+    """ARIANN_TIMEOUT_MS, as in runtime.py:36-37."""
+    return int(os.environ.get("ARIANN_TIMEOUT_MS", DEFAULT_TIMEOUT_MS)) / 1000.0
+
+
+class SessionAbort(RuntimeError):
+    """Protocol aborted: peer failure, timeout, or frame desync (runtime.py:40-41)."""
+
+
+@dataclass
+class Frame:
+    """One message: a tag and a device (or host) tensor payload."""
+
+    tag: int
+    payload: torch.Tensor
+    event: object = None  # torch.cuda.Event ordering the payload on the sender's stream
+
+
+@dataclass
+class RoundLedger:
+    """Per-operation counters of online rounds, bytes, and elements (runtime.py:66-96)."""
+
+    rounds: dict = field(default_factory=dict)
+    bytes_sent: dict = field(default_factory=dict)
+    bytes_received: dict = field(default_factory=dict)
+    elements: dict = field(default_factory=dict)
+
+    def record(self, op: str, sent: int, received: int, elements: int):
+        self.rounds[op] = self.rounds.get(op, 0) + 1
+        self.bytes_sent[op] = self.bytes_sent.get(op, 0) + sent
+        self.bytes_received[op] = self.bytes_received.get(op, 0) + received
+        self.elements[op] = self.elements.get(op, 0) + elements
+
+    def total_rounds(self) -> int:
+        return sum(self.rounds.values())
+
+    def total_bytes_sent(self) -> int:
+        return sum(self.bytes_sent.values())
+
+    def as_dict(self) -> dict:
+        return {"rounds": dict(self.rounds), "bytes_sent": dict(self.bytes_sent),
+                "bytes_received": dict(self.bytes_received), "elements": dict(self.elements)}
+
+    def snapshot(self) -> dict:
+        return {op: n for op, n in self.rounds.items()}
+
+
+def _nbytes(t: torch.Tensor) -> int:
+    return t.numel() * t.element_size()
+
+
+# ---------------------------------------------------------------------------
+# Transports
+# ---------------------------------------------------------------------------
+
+class LocalTransport:
+    """In-process duplex channel: FIFO queues of device-tensor frames (runtime.py:103-133)."""
+
+    def __init__(self, inbox: queue.Queue, outbox: queue.Queue):
+        self._inbox = inbox
+        self._outbox = outbox
+        self._closed = False
+
+    def send(self, frame: Frame):
+        if self._closed:
+            raise SessionAbort("transport closed")
+        p = frame.payload
+        if frame.event is None and isinstance(p, torch.Tensor) and p.is_cuda:
+            ev = torch.cuda.Event()
+            ev.record(torch.cuda.current_stream(p.device))
+            frame = Frame(frame.tag, p, ev)
+        self._outbox.put(frame)
+
+    def recv(self) -> Frame:
+        try:
+            frame = self._inbox.get(timeout=timeout_seconds())
+        except queue.Empty:
+            raise SessionAbort("timed out waiting for peer") from None
+        if frame is None:
+            raise SessionAbort("peer closed the channel")
+        if frame.event is not None:
+            cur = torch.cuda.current_stream(frame.payload.device)
+            cur.wait_event(frame.event)
+            # the sender's allocator must not recycle the buffer before we read it
+            frame.payload.record_stream(cur)
+        return frame
+
+    def close(self):
+        if not self._closed:
+            self._closed = True
+            self._outbox.put(None)
+
+
+def local_pair() -> tuple[LocalTransport, LocalTransport]:
+    a, b = queue.Queue(), queue.Queue()
+    return LocalTransport(a, b), LocalTransport(b, a)
+
+
+_DTYPES = [torch.uint8, torch.int16, torch.int32, torch.int64, torch.uint16, torch.uint32,
+           torch.uint64]
+_DTYPE_CODE = {d: i for i, d in enumerate(_DTYPES)}
+# NCCL / gloo move bytes; unsigned payloads travel as their signed views
+_SIGNED = {torch.uint16: torch.int16, torch.uint32: torch.int32, torch.uint64: torch.int64}
+
+
+class DistTransport:
+    """One party per process over torch.distributed point-to-point.
+
+    ``peer`` is the other party's global rank; ``group`` optionally restricts
+    the communicator (e.g. a 2-rank pair inside an 8-GPU job). NCCL carries
+    device tensors over NVLink / NVSwitch; gloo (CPU tensors) is used by the
+    multi-process CPU tests.
+    """
+
+    def __init__(self, peer: int, group=None, device=None):
+        import torch.distributed as dist
+        self._dist = dist
+        self.peer = peer
+        self.group = group
+        self.device = torch.device(device) if device is not None else (
+            torch.device("cuda", torch.cuda.current_device())
+            if dist.get_backend(group) == "nccl" else torch.device("cpu"))
+        self._closed = False
+
+    def _wire(self, t: torch.Tensor) -> torch.Tensor:
+        t = t.contiguous()
+        return t.view(_SIGNED[t.dtype]) if t.dtype in _SIGNED else t
+
+    def exchange_frames(self, frame: Frame) -> Frame:
+        """Send our frame and receive the peer's (both directions in one batch)."""
+        if self._closed:
+            raise SessionAbort("transport closed")
+        dist = self._dist
+        p = frame.payload.to(self.device)
+        hdr = torch.tensor([frame.tag, _DTYPE_CODE[p.dtype], p.numel()], dtype=torch.int64,
+                           device=self.device)
+        peer_hdr = torch.empty(3, dtype=torch.int64, device=self.device)
+        ops = [dist.P2POp(dist.isend, hdr, self.peer, self.group),
+               dist.P2POp(dist.irecv, peer_hdr, self.peer, self.group)]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        tag, code, numel = (int(v) for v in peer_hdr.tolist())
+        if tag == FRAME_ABORT:
+            raise SessionAbort("peer aborted")
+        if code < 0 or code >= len(_DTYPES):
+            raise SessionAbort("corrupt frame header")
+        out = torch.empty(numel, dtype=_DTYPES[code], device=self.device)
+        ops = []
+        if p.numel():
+            ops.append(dist.P2POp(dist.isend, self._wire(p).reshape(-1), self.peer, self.group))
+        if numel:
+            ops.append(dist.P2POp(dist.irecv, self._wire(out), self.peer, self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        return Frame(tag, out)
+
+    def send_abort(self):
+        # best effort: the peer sees FRAME_ABORT in its next header
+        try:
+            self.exchange_frames(Frame(FRAME_ABORT, torch.empty(0, dtype=torch.uint8)))
+        except Exception:  # noqa: BLE001
+            pass
+
+    def close(self):
+        self._closed = True
+
+
+# ---------------------------------------------------------------------------
+# Session
+# ---------------------------------------------------------------------------
+
+class Session:
+    """One party's end of an online 2-party computation (runtime.py:217-282)."""
+
+    def __init__(self, party: int, transport):
+        if party not in (0, 1):
+            raise ValueError("party must be 0 or 1")
+        self.party = party
+        self.transport = transport
+        self.ledger = RoundLedger()
+        self.open = True
+
+    def exchange(self, op: str, tag: int, payload: torch.Tensor, elements: int) -> torch.Tensor:
+        """Send one frame and receive the peer's matching frame (one round).
+
+        ``payload`` is a tensor (normally the device wire buffer); the peer's
+        payload comes back as a tensor on the same device, stream-ordered."""
+        if not self.open:
+            raise SessionAbort("session is closed")
+        if tag not in _FRAME_TAGS:
+            raise ValueError(f"unknown frame tag {tag}")
+        frame = Frame(tag, payload)
+        try:
+            if isinstance(self.transport, DistTransport):
+                peer = self.transport.exchange_frames(frame)
+            else:
+                self.transport.send(frame)
+                peer = self.transport.recv()
+        except SessionAbort:
+            self.open = False
+            raise
+        if peer.tag == FRAME_ABORT:
+            self.open = False
+            raise SessionAbort("peer aborted")
+        if peer.tag != tag:
+            self.open = False
+            raise SessionAbort(f"frame desync: expected tag {tag}, got {peer.tag}")
+        self.ledger.record(op, _nbytes(payload), _nbytes(peer.payload), elements)
+        return peer.payload
+
+    def abort(self, reason: str = ""):
+        if self.open:
+            try:
+                if isinstance(self.transport, DistTransport):
+                    self.transport.send_abort()
+                else:
+                    self.transport.send(Frame(FRAME_ABORT, torch.empty(0, dtype=torch.uint8)))
+            except Exception:  # noqa: BLE001
+                pass
+            self.open = False
+
+    def close(self):
+        self.open = False
+        self.transport.close()
+
+
+def run_session(party: int, transport, program):
+    """Run ``program(session)``; returns (result, ledger) (runtime.py:272-282)."""
+    session = Session(party, transport)
+    try:
+        result = program(session)
+    except Exception:
+        session.abort("program failed")
+        raise
+    finally:
+        session.close()
+    return result, session.ledger
+
+
+def run_local_pair(program0, program1=None, device=None):
+    """Two programs over the in-process transport, one thread per party
+    (runtime.py:285-311). Each party thread runs on its own CUDA stream of
+    ``device`` so the two parties' kernels can overlap; the exchange orders
+    them. Returns ((result0, ledger0), (result1, ledger1))."""
+    if program1 is None:
+        program1 = program0
+    t0, t1 = local_pair()
+    results = [None, None]
+    errors = [None, None]
+    dev = None
+    if torch.cuda.is_available():
+        dev = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        parent = torch.cuda.current_stream(dev)
+        streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+        for s in streams:
+            s.wait_stream(parent)
+
+    def runner(party, transport, program):
+        try:
+            if dev is not None:
+                with torch.cuda.device(dev), torch.cuda.stream(streams[party]):
+                    results[party] = run_session(party, transport, program)
+            else:
+                results[party] = run_session(party, transport, program)
+        except BaseException as exc:  # propagate to the caller
+            errors[party] = exc
+            transport.close()
+
+    th0 = threading.Thread(target=runner, args=(0, t0, program0))
+    th1 = threading.Thread(target=runner, args=(1, t1, program1))
+    th0.start(); th1.start()
+    th0.join(); th1.join()
+    if dev is not None:
+        for s in streams:
+            parent.wait_stream(s)
+    for err in errors:
+        if err is not None:
+            raise err
+    return results[0], results[1]
+
+
+def run_dist_party(party: int, peer: int, program, group=None, device=None):
+    """This process plays ``party`` against the process of global rank ``peer``."""
+    return run_session(party, DistTransport(peer, group, device), program)
