@@ -19,7 +19,18 @@
 #include <stdint.h>
 #include "aes_consts.h"
 
+#ifndef FSSB_IMAD_ADDR
+#define FSSB_IMAD_ADDR 0
+#endif
+
 namespace fssb {
+
+#if FSSB_IMAD_ADDR
+// Multipliers read from the constant bank so ptxas cannot strength-reduce the
+// IMADs below into ALU shifts: the address arithmetic of table bytes 0 and 3
+// runs on the (otherwise idle) FMA pipe instead of the ALU pipe.
+static __constant__ uint32_t kAddrMul[3] = {1u << 24, 1u << 16, 1u << 8};
+#endif
 
 constexpr int kTableWords = 32768;            // 4 tables x 256 entries x 32 lanes
 constexpr int kTableBytes = kTableWords * 4;  // 128 KiB dynamic shared memory
@@ -57,7 +68,22 @@ __device__ __forceinline__ Tab make_tab(const uint32_t* tab) {
 // Table J (0..3) looked up at byte K (0..3) of column c.
 template <int J, int K>
 __device__ __forceinline__ uint32_t T(const Tab& tb, uint32_t c) {
-    const uint32_t addr = __byte_perm(c, (J & 1) ? tb.lo1 : tb.lo0, 0x5504 + 0x10 * K);
+    const uint32_t lo = (J & 1) ? tb.lo1 : tb.lo0;
+    uint32_t addr;
+#if FSSB_IMAD_ADDR
+    if (K == 0) {         // addr = ((c << 24) * 2^16) >> 32 + lo = byte0 << 8 | lo
+        uint32_t t;
+        asm("mul.lo.u32 %0, %1, %2;" : "=r"(t) : "r"(c), "r"(kAddrMul[0]));
+        asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(t), "r"(kAddrMul[1]), "r"(lo));
+    } else if (K == 3) {  // addr = (c * 2^8) >> 32 = byte3, then * 2^8 + lo
+        uint32_t t;
+        asm("mul.hi.u32 %0, %1, %2;" : "=r"(t) : "r"(c), "r"(kAddrMul[2]));
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(t), "r"(kAddrMul[2]), "r"(lo));
+    } else
+#endif
+    {
+        addr = __byte_perm(c, lo, 0x5504 + 0x10 * K);
+    }
     return *reinterpret_cast<const uint32_t*>(tb.base + (J >> 1) * kRegion1 + addr);
 }
 

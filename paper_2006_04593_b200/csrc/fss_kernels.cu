@@ -26,7 +26,10 @@ using fssb::U4;
 
 namespace {
 
-constexpr int kThreads = 512;
+#ifndef FSSB_THREADS
+#define FSSB_THREADS 512
+#endif
+constexpr int kThreads = FSSB_THREADS;
 
 __device__ __forceinline__ uint64_t ring_mask(int w) { return w >= 64 ? ~0ULL : ((1ULL << w) - 1); }
 

@@ -15,7 +15,7 @@
 namespace {
 
 constexpr int kProbeThreads = 512;
-constexpr int kTabWords = 256 * 32;  // one table, lane-replicated
+constexpr int kTabWords = 256 * 64;  // two interleaved lane-replicated tables (64 KiB)
 
 __device__ __forceinline__ uint64_t gtimer() {
     uint64_t t;
@@ -26,7 +26,7 @@ __device__ __forceinline__ uint64_t gtimer() {
 __global__ void __launch_bounds__(kProbeThreads, 1)
 lds_probe_kernel(int iters, uint32_t seed, uint32_t* sink, unsigned long long* cycles,
                  unsigned long long* ns) {
-    __shared__ uint32_t tab[kTabWords];
+    extern __shared__ uint32_t tab[];
     for (int i = threadIdx.x; i < kTabWords; i += blockDim.x) tab[i] = (uint32_t)(i * 2654435761u);
     __syncthreads();
     const uint32_t lo = (threadIdx.x & 31) * 4;
@@ -86,6 +86,7 @@ extern "C" int fss_probe_peaks(fss_peaks* out) {
     if (cudaMalloc(&sink, 4096 * sizeof(uint32_t)) != cudaSuccess ||
         cudaMalloc(&meta, 2 * sizeof(unsigned long long)) != cudaSuccess)
         return fssb::set_error(FSS_ECUDA, "probe allocation failed");
+    cudaFuncSetAttribute(lds_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTabWords * 4);
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const int lds_iters = 80000, lop_iters = 100000;
@@ -94,7 +95,7 @@ extern "C" int fss_probe_peaks(fss_peaks* out) {
     for (int rep = 0; rep < 3; rep++) {  // first rep warms clocks up; keep the best
         cudaMemset(meta, 0, 2 * sizeof(unsigned long long));
         cudaEventRecord(e0);
-        lds_probe_kernel<<<sms, kProbeThreads>>>(lds_iters, 7u + rep, sink, meta, meta + 1);
+        lds_probe_kernel<<<sms, kProbeThreads, kTabWords * 4>>>(lds_iters, 7u + rep, sink, meta, meta + 1);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float t = 0.f;

@@ -127,17 +127,16 @@ def maxpool_k2(session, x: AdditiveShare, prep: MaxpoolK2Prep) -> AdditiveShare:
     """k=2 max pooling as a two-level max tree, max(a, b) = b + ReLU(a - b);
     four rounds (nn_ops.py:179-190)."""
     win, lead, side = _windows(x, 2, 2)
-    flat = win.reshape(-1, 4)
-    w = AdditiveShare(x.party, RingTensor(flat, x.n_bits, _trusted=True), x.precision)
-    lhs = AdditiveShare(x.party, RingTensor(flat[:, [0, 2]].contiguous(), x.n_bits, _trusted=True),
-                        x.precision)
-    rhs = AdditiveShare(x.party, RingTensor(flat[:, [1, 3]].contiguous(), x.n_bits, _trusted=True),
-                        x.precision)
-    del w
+    flat = _dev.as_i64(win.reshape(-1, 4))
+    lhs = AdditiveShare(x.party, RingTensor(_dev.as_u64(flat[:, [0, 2]].contiguous()), x.n_bits,
+                                            _trusted=True), x.precision)
+    rhs = AdditiveShare(x.party, RingTensor(_dev.as_u64(flat[:, [1, 3]].contiguous()), x.n_bits,
+                                            _trusted=True), x.precision)
     mx = rhs + relu(session, lhs - rhs, prep.level1)
-    a = AdditiveShare(x.party, RingTensor(mx.values.data[:, 0].contiguous(), x.n_bits,
+    m2 = _dev.as_i64(mx.values.data)
+    a = AdditiveShare(x.party, RingTensor(_dev.as_u64(m2[:, 0].contiguous()), x.n_bits,
                                           _trusted=True), x.precision)
-    b = AdditiveShare(x.party, RingTensor(mx.values.data[:, 1].contiguous(), x.n_bits,
+    b = AdditiveShare(x.party, RingTensor(_dev.as_u64(m2[:, 1].contiguous()), x.n_bits,
                                           _trusted=True), x.precision)
     out = b + relu(session, a - b, prep.level2)
     return out.reshape(*lead, side, side)
