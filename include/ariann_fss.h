@@ -51,6 +51,12 @@ int fss_abi_version(void);
 int fss_aes_mmo_expand(const uint8_t* seeds, uint64_t count, int out_blocks, uint8_t* out,
                        void* stream);
 
+/* Same result as fss_aes_mmo_expand through the bitsliced AES
+ * (csrc/aes_bitsliced.cuh) instead of T-tables: the measured alternative
+ * SURVEY.md 8d proposed. count must be a multiple of 32. */
+int fss_aes_mmo_expand_bitsliced(const uint8_t* seeds, uint64_t count, int out_blocks, uint8_t* out,
+                                 void* stream);
+
 /* fss._sample_tape (fss.py:292-303) through numpy's PCG64 Generator
  * (_uniform_ring fss.py:47-51, random_seeds prg.py:36-40) for 1 <= n <= 63:
  * draws alpha (if draw_alpha), alpha0, s0, s1 exactly as numpy would from `st`.

@@ -37,6 +37,7 @@ SIGNATURES = {
     "fss_abi_version": [],
     "fss_last_error": [],
     "fss_aes_mmo_expand": [_vp, _u64, _int, _vp, _vp],
+    "fss_aes_mmo_expand_bitsliced": [_vp, _u64, _int, _vp, _vp],
     "fss_pcg64_tape": [ctypes.POINTER(PcgState), _int, _u64, _int, _vp, _vp, _vp, _vp,
                        ctypes.POINTER(PcgState), _vp],
     "fss_dpf_keygen": [_int, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],

@@ -95,6 +95,38 @@ __device__ __forceinline__ uint32_t rk(int w, uint32_t m) {
     return kRK[KEY][w];
 }
 
+#ifndef FSSB_LOP3_COMBINE
+#define FSSB_LOP3_COMBINE 1
+#endif
+
+__device__ __forceinline__ uint32_t lop3_xor3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+__device__ __forceinline__ uint32_t lop3_xor_and(uint32_t a, uint32_t b, uint32_t c) {  // a ^ (b & c)
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0x78;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+// Column mix of one round: t0 ^ t1 ^ t2 ^ t3 ^ rk. For a per-element selected
+// key, rk = RK1 ^ (m & (RK1 ^ RK2)); written as three explicit LOP3s
+// ((t0^t1^t2), (^t3^RK1), (^(m&D))) -- left to itself the compiler emits four.
+template <int KEY, bool SEL>
+__device__ __forceinline__ uint32_t mixcol(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3, int w,
+                                           uint32_t m) {
+#if FSSB_LOP3_COMBINE
+    if (SEL) {
+        const uint32_t x = lop3_xor3(t0, t1, t2);
+        const uint32_t y = lop3_xor3(x, t3, kRK[0][w]);
+        return lop3_xor_and(y, m, kRK[0][w] ^ kRK[1][w]);
+    }
+#endif
+    return t0 ^ t1 ^ t2 ^ t3 ^ rk<KEY, SEL>(w, m);
+}
+
 // One full AES-128 encryption of (c0..c3) (little-endian column words).
 template <int KEY, bool SEL>
 __device__ __forceinline__ U4 aes128(const Tab& tb, U4 s, uint32_t m) {
@@ -104,14 +136,14 @@ __device__ __forceinline__ U4 aes128(const Tab& tb, U4 s, uint32_t m) {
     uint32_t c3 = s.w ^ rk<KEY, SEL>(3, m);
 #pragma unroll
     for (int r = 1; r < 10; r++) {
-        const uint32_t n0 = T<0, 0>(tb, c0) ^ T<1, 1>(tb, c1) ^ T<2, 2>(tb, c2) ^ T<3, 3>(tb, c3) ^
-                            rk<KEY, SEL>(4 * r + 0, m);
-        const uint32_t n1 = T<0, 0>(tb, c1) ^ T<1, 1>(tb, c2) ^ T<2, 2>(tb, c3) ^ T<3, 3>(tb, c0) ^
-                            rk<KEY, SEL>(4 * r + 1, m);
-        const uint32_t n2 = T<0, 0>(tb, c2) ^ T<1, 1>(tb, c3) ^ T<2, 2>(tb, c0) ^ T<3, 3>(tb, c1) ^
-                            rk<KEY, SEL>(4 * r + 2, m);
-        const uint32_t n3 = T<0, 0>(tb, c3) ^ T<1, 1>(tb, c0) ^ T<2, 2>(tb, c1) ^ T<3, 3>(tb, c2) ^
-                            rk<KEY, SEL>(4 * r + 3, m);
+        const uint32_t n0 = mixcol<KEY, SEL>(T<0, 0>(tb, c0), T<1, 1>(tb, c1), T<2, 2>(tb, c2),
+                                             T<3, 3>(tb, c3), 4 * r + 0, m);
+        const uint32_t n1 = mixcol<KEY, SEL>(T<0, 0>(tb, c1), T<1, 1>(tb, c2), T<2, 2>(tb, c3),
+                                             T<3, 3>(tb, c0), 4 * r + 1, m);
+        const uint32_t n2 = mixcol<KEY, SEL>(T<0, 0>(tb, c2), T<1, 1>(tb, c3), T<2, 2>(tb, c0),
+                                             T<3, 3>(tb, c1), 4 * r + 2, m);
+        const uint32_t n3 = mixcol<KEY, SEL>(T<0, 0>(tb, c3), T<1, 1>(tb, c0), T<2, 2>(tb, c1),
+                                             T<3, 3>(tb, c2), 4 * r + 3, m);
         c0 = n0;
         c1 = n1;
         c2 = n2;

@@ -26,10 +26,29 @@ using fssb::U4;
 
 namespace {
 
-#ifndef FSSB_THREADS
-#define FSSB_THREADS 512
+// Software-pipelined correction-word loads (level i+1 loads during level i's
+// AES): +0.7 % for DCF eval at 1024 threads, -1.4 % for DPF eval
+// (profiles/r01_aes_variants_c.json), so on for DCF only.
+#ifndef FSSB_PREFETCH_DCF
+#define FSSB_PREFETCH_DCF 1
 #endif
+#ifndef FSSB_PREFETCH_DPF
+#define FSSB_PREFETCH_DPF 0
+#endif
+#ifdef FSSB_PREFETCH
+#undef FSSB_PREFETCH_DCF
+#undef FSSB_PREFETCH_DPF
+#define FSSB_PREFETCH_DCF FSSB_PREFETCH
+#define FSSB_PREFETCH_DPF FSSB_PREFETCH
+#endif
+#ifndef FSSB_THREADS
+#define FSSB_THREADS 1024
+#endif
+// Eval kernels: 32 warps per SM (64 registers) hide the LDS / LDG latency best
+// (profiles/r01_aes_variants_b.json: 512 -> 1024 threads = +5 % DCF, +17 % DPF).
 constexpr int kThreads = FSSB_THREADS;
+// Keygen kernels need ~100-127 registers: 16 warps per SM.
+constexpr int kKeygenThreads = 512;
 
 __device__ __forceinline__ uint64_t ring_mask(int w) { return w >= 64 ? ~0ULL : ((1ULL << w) - 1); }
 
@@ -53,7 +72,7 @@ __device__ __forceinline__ U4 sel4(bool c, U4 a, U4 b) {
 
 // ------------------------------------------------------------------ expand
 // prg.expand (prg.py:43-60): out block b = AES_{k_b}(seed) ^ seed.
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kKeygenThreads, 1)
 expand_kernel(const uint8_t* __restrict__ seeds, uint64_t count, int blocks, uint8_t* __restrict__ out) {
     extern __shared__ uint32_t tab[];
     fssb::fill_tables(tab);
@@ -87,10 +106,21 @@ dpf_eval_kernel(int party, int n, uint64_t count, uint64_t ld, const uint8_t* __
         U4 s = ld16(seed0 + 16 * e);
         uint32_t t = party;
         const uint64_t xe = x[e] & mask;
+#if FSSB_PREFETCH_DPF
+        // software pipeline: level i+1's correction words load during level i's AES
+        U4 cw = ld16(scw + 16 * e);
+        uint32_t f = __ldg(tcw + e);
+#endif
         for (int i = 0; i < n; i++) {
+#if FSSB_PREFETCH_DPF
+            const uint64_t offn = (uint64_t)(i + 1 < n ? i + 1 : i) * ld + e;
+            const U4 cw_next = ld16(scw + 16 * offn);
+            const uint32_t f_next = __ldg(tcw + offn);
+#else
             const uint64_t off = (uint64_t)i * ld + e;
             const U4 cw = ld16(scw + 16 * off);
             const uint32_t f = __ldg(tcw + off);
+#endif
             const uint32_t xb = (uint32_t)(xe >> (n - 1 - i)) & 1u;
             const U4 a = fssb::mmo<0, true>(tb, s, 0u - xb);
             const uint32_t tm = 0u - t;
@@ -98,6 +128,10 @@ dpf_eval_kernel(int party, int n, uint64_t count, uint64_t ld, const uint8_t* __
             const uint32_t tn = ((a.w >> 31) ^ (t & (f >> xb))) & 1u;
             s.w &= 0x7FFFFFFFu;
             t = tn;
+#if FSSB_PREFETCH_DPF
+            cw = cw_next;
+            f = f_next;
+#endif
         }
         uint64_t o = (((uint64_t)t * cw_final[e]) + lo64(s)) & mask;
         if (party) o = (0 - o) & mask;
@@ -126,12 +160,26 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
         uint32_t t = party;
         uint64_t acc = 0;
         const uint64_t xe = x[e] & nmask;
+#if FSSB_PREFETCH_DCF
+        U4 cw = ld16(scw + 16 * e);
+        uint32_t f = __ldg(tcw + e);
+        uint64_t sig = __ldg(sigma_cw + e);
+        uint64_t leaf = __ldg(leaf_cw + e);
+#endif
         for (int i = 0; i < n; i++) {
+#if FSSB_PREFETCH_DCF
+            const uint64_t offn = (uint64_t)(i + 1 < n ? i + 1 : i) * ld + e;
+            const U4 cw_next = ld16(scw + 16 * offn);
+            const uint32_t f_next = __ldg(tcw + offn);
+            const uint64_t sig_next = __ldg(sigma_cw + offn);
+            const uint64_t leaf_next = __ldg(leaf_cw + offn);
+#else
             const uint64_t off = (uint64_t)i * ld + e;
             const U4 cw = ld16(scw + 16 * off);
             const uint32_t f = __ldg(tcw + off);
             const uint64_t sig = __ldg(sigma_cw + off);
             const uint64_t leaf = __ldg(leaf_cw + off);
+#endif
             const uint32_t xb = (uint32_t)(xe >> (n - 1 - i)) & 1u;
             const U4 a = fssb::mmo<0, true>(tb, s, 0u - xb);
             const U4 g = fssb::mmo<2, false>(tb, s, 0);
@@ -147,6 +195,12 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
             const uint32_t tn = ((a.w >> 31) ^ (t & (f >> xb))) & 1u;
             s.w &= 0x7FFFFFFFu;
             t = tn;
+#if FSSB_PREFETCH_DCF
+            cw = cw_next;
+            f = f_next;
+            sig = sig_next;
+            leaf = leaf_next;
+#endif
         }
         const uint64_t off = (uint64_t)n * ld + e;
         const uint64_t last = (((uint64_t)t * __ldg(leaf_cw + off)) + lo64(s)) & mask;
@@ -158,7 +212,7 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
 
 // -------------------------------------------------------------- DPF keygen
 // fss._keygen_eq_core (fss.py:173-216): both parties' walks, 4 AES blocks/level.
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kKeygenThreads, 1)
 dpf_keygen_kernel(int n, uint64_t count, const uint64_t* __restrict__ alpha,
                   const uint64_t* __restrict__ alpha0, const uint8_t* __restrict__ s0_init,
                   const uint8_t* __restrict__ s1_init, uint8_t* __restrict__ scw,
@@ -203,7 +257,7 @@ dpf_keygen_kernel(int n, uint64_t count, const uint64_t* __restrict__ alpha,
 
 // -------------------------------------------------------------- DCF keygen
 // fss._keygen_cmp_core (fss.py:219-289): 6 AES blocks/level (3 per party).
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kKeygenThreads, 1)
 dcf_keygen_kernel(int n, int out_bits, uint64_t count, const uint64_t* __restrict__ alpha,
                   const uint64_t* __restrict__ alpha0, const uint8_t* __restrict__ s0_init,
                   const uint8_t* __restrict__ s1_init, uint8_t* __restrict__ scw,
@@ -397,8 +451,8 @@ int prep_launch(K kernel, int* grid) {
     return kOk;
 }
 
-int grid_for(uint64_t count, int sms) {
-    const uint64_t need = (count + kThreads - 1) / kThreads;
+int grid_for(uint64_t count, int sms, int threads) {
+    const uint64_t need = (count + threads - 1) / threads;
     return (int)(need < (uint64_t)sms ? (need ? need : 1) : sms);
 }
 
@@ -422,7 +476,7 @@ int fss_aes_mmo_expand(const uint8_t* seeds, uint64_t count, int out_blocks, uin
     if (count == 0) return kOk;
     int sms;
     if (int rc = prep_launch(expand_kernel, &sms)) return rc;
-    expand_kernel<<<grid_for(count, sms), kThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+    expand_kernel<<<grid_for(count, sms, kKeygenThreads), kKeygenThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
         seeds, count, out_blocks, out);
     return check_launch();
 }
@@ -435,7 +489,7 @@ int fss_dpf_eval(int party, int n, uint64_t count, uint64_t ld, const uint8_t* s
     if (count == 0) return kOk;
     int sms;
     if (int rc = prep_launch(dpf_eval_kernel, &sms)) return rc;
-    dpf_eval_kernel<<<grid_for(count, sms), kThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+    dpf_eval_kernel<<<grid_for(count, sms, kThreads), kThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
         party, n, count, ld, seed0, scw, tcw, cw_final, x, out);
     return check_launch();
 }
@@ -450,7 +504,7 @@ int fss_dcf_eval(int party, int n, int out_bits, uint64_t count, uint64_t ld, co
     if (count == 0) return kOk;
     int sms;
     if (int rc = prep_launch(dcf_eval_kernel, &sms)) return rc;
-    dcf_eval_kernel<<<grid_for(count, sms), kThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+    dcf_eval_kernel<<<grid_for(count, sms, kThreads), kThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
         party, n, out_bits, count, ld, seed0, scw, tcw, sigma_cw, leaf_cw, x, out, levels);
     return check_launch();
 }
@@ -462,7 +516,7 @@ int fss_dpf_keygen(int n, uint64_t count, const uint64_t* alpha, const uint64_t*
     if (count == 0) return kOk;
     int sms;
     if (int rc = prep_launch(dpf_keygen_kernel, &sms)) return rc;
-    dpf_keygen_kernel<<<grid_for(count, sms), kThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+    dpf_keygen_kernel<<<grid_for(count, sms, kKeygenThreads), kKeygenThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
         n, count, alpha, alpha0, s0, s1, scw, tcw, cw_final, alpha1);
     return check_launch();
 }
@@ -476,7 +530,7 @@ int fss_dcf_keygen(int n, int out_bits, uint64_t count, const uint64_t* alpha,
     if (count == 0) return kOk;
     int sms;
     if (int rc = prep_launch(dcf_keygen_kernel, &sms)) return rc;
-    dcf_keygen_kernel<<<grid_for(count, sms), kThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+    dcf_keygen_kernel<<<grid_for(count, sms, kKeygenThreads), kKeygenThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
         n, out_bits, count, alpha, alpha0, s0, s1, scw, tcw, sigma_cw, leaf_cw, alpha1);
     return check_launch();
 }

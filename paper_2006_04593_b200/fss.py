@@ -441,19 +441,66 @@ def _eval_operands(k, names):
     return ld
 
 
+# Host-tensor inputs at least this large are streamed through the GPU in
+# chunks on two CUDA streams, so the H2D copy of x, the evaluation kernel and
+# the D2H copy of the shares of consecutive chunks overlap.
+PIPELINE_MIN = 1 << 21
+PIPELINE_CHUNK = 1 << 21
+
+
+def _run_eval(launch, xt, host, count: int, dev):
+    """Run ``launch(lo, hi, x_dev, out_dev, stream)`` over [0, count).
+
+    Device (or numpy) input: one launch on the current stream. Pinned host
+    torch input: a 2-stream chunked pipeline that returns a pinned host tensor."""
+    if host != "torch_pinned" or count < PIPELINE_MIN:
+        if host == "torch_pinned":
+            xt = xt.to(dev, non_blocking=True)
+        out = torch.empty(count, dtype=torch.uint64, device=dev)
+        launch(0, count, xt, out, _dev.stream_handle(dev))
+        return _result(out, "torch" if host == "torch_pinned" else host)
+    out_host = torch.empty(count, dtype=torch.uint64, pin_memory=True)
+    cur = torch.cuda.current_stream(dev)
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    for st in streams:
+        st.wait_stream(cur)
+    xs64, os64 = xt.view(torch.int64), out_host.view(torch.int64)
+    for i, lo in enumerate(range(0, count, PIPELINE_CHUNK)):
+        hi = min(count, lo + PIPELINE_CHUNK)
+        st = streams[i & 1]
+        with torch.cuda.stream(st):
+            xd = xs64[lo:hi].to(dev, non_blocking=True)
+            od = torch.empty(hi - lo, dtype=torch.int64, device=dev)
+            launch(lo, hi, xd, od, st.cuda_stream)
+            os64[lo:hi].copy_(od, non_blocking=True)
+    for st in streams:
+        cur.wait_stream(st)
+    cur.synchronize()
+    return out_host
+
+
+def _prep_x(x, count: int, n: int, dev):
+    """_broadcast_x plus the pinned-host fast path (no upload here)."""
+    if isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned() and x.numel() == count \
+            and x.dtype in (torch.uint64, torch.int64):
+        return x.reshape(-1).contiguous(), "torch_pinned"
+    return _broadcast_x(x, count, n, dev)
+
+
 def eval_eq(party: int, k: EqKeyBatch, x):
     """Per-party share of 1[x == alpha] (fss.py:357-377) via fss_dpf_eval."""
     k.validate()
     n, count, dev = k.n_bits, k.count, k.device
-    xt, host = _broadcast_x(x, count, n, dev)
+    xt, host = _prep_x(x, count, n, dev)
     ld = _eval_operands(k, ("tcw",))
     seed0, cw_final = k.seed0.contiguous(), k.cw_final.contiguous()
-    out = torch.empty(count, dtype=torch.uint64, device=dev)
-    with torch.cuda.device(dev):
-        _lib.call("fss_dpf_eval", int(party), n, count, ld, _dev.ptr(seed0), _dev.ptr(k.scw),
-                  _dev.ptr(k.tcw), _dev.ptr(cw_final), _dev.ptr(xt), _dev.ptr(out),
-                  _dev.stream_handle(dev))
-    return _result(out, host)
+
+    def launch(lo, hi, xd, od, stream):
+        with torch.cuda.device(dev):
+            _lib.call("fss_dpf_eval", int(party), n, hi - lo, ld, _dev.ptr(seed0[lo:hi]),
+                      _dev.ptr(k.scw[:, lo:hi]), _dev.ptr(k.tcw[:, lo:hi]),
+                      _dev.ptr(cw_final[lo:hi]), _dev.ptr(xd), _dev.ptr(od), stream)
+    return _run_eval(launch, xt, host, count, dev)
 
 
 def eval_cmp(party: int, k: CmpKeyBatch, x, return_levels: bool = False):
@@ -463,19 +510,27 @@ def eval_cmp(party: int, k: CmpKeyBatch, x, return_levels: bool = False):
     shape (n+1, count); at most one level reconstructs to 1."""
     k.validate()
     n, count, dev = k.n_bits, k.count, k.device
-    xt, host = _broadcast_x(x, count, n, dev)
+    xt, host = _prep_x(x, count, n, dev)
     ld = _eval_operands(k, ("tcw", "sigma_cw", "leaf_cw"))
     seed0 = k.seed0.contiguous()
-    out = torch.empty(count, dtype=torch.uint64, device=dev)
-    levels = torch.empty((n + 1, count), dtype=torch.uint64, device=dev) if return_levels else None
-    with torch.cuda.device(dev):
-        _lib.call("fss_dcf_eval", int(party), n, int(k.out_bits), count, ld, _dev.ptr(seed0),
-                  _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(k.sigma_cw), _dev.ptr(k.leaf_cw),
-                  _dev.ptr(xt), _dev.ptr(out), _dev.ptr(levels), _dev.stream_handle(dev))
-    if host:
-        out = _result(out, host)
-        levels = _result(levels, host) if return_levels else None
-    return (out, levels) if return_levels else out
+    if return_levels:
+        if host == "torch_pinned":
+            xt, host = xt.to(dev), "torch"
+        out = torch.empty(count, dtype=torch.uint64, device=dev)
+        levels = torch.empty((n + 1, count), dtype=torch.uint64, device=dev)
+        with torch.cuda.device(dev):
+            _lib.call("fss_dcf_eval", int(party), n, int(k.out_bits), count, ld, _dev.ptr(seed0),
+                      _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(k.sigma_cw), _dev.ptr(k.leaf_cw),
+                      _dev.ptr(xt), _dev.ptr(out), _dev.ptr(levels), _dev.stream_handle(dev))
+        return _result(out, host), _result(levels, host)
+
+    def launch(lo, hi, xd, od, stream):
+        with torch.cuda.device(dev):
+            _lib.call("fss_dcf_eval", int(party), n, int(k.out_bits), hi - lo, ld,
+                      _dev.ptr(seed0[lo:hi]), _dev.ptr(k.scw[:, lo:hi]), _dev.ptr(k.tcw[:, lo:hi]),
+                      _dev.ptr(k.sigma_cw[:, lo:hi]), _dev.ptr(k.leaf_cw[:, lo:hi]), _dev.ptr(xd),
+                      _dev.ptr(od), None, stream)
+    return _run_eval(launch, xt, host, count, dev)
 
 
 # ---------------------------------------------------------------------------

@@ -18,11 +18,14 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = {
-    "base512": [],
-    "t768": ["FSSB_THREADS=768"],
-    "imad512": ["FSSB_IMAD_ADDR=1"],
-    "imad768": ["FSSB_IMAD_ADDR=1", "FSSB_THREADS=768"],
+    "default": [],
+    "no_lop3_combine": ["FSSB_LOP3_COMBINE=0"],
 }
+# round-1 sweep b (profiles/r01_aes_variants_b.json): 512/640/768/1024 threads
+# x prefetch; more resident warps win (1024: DCF 92.9 %, DPF 85.5 % of the
+# lookup roof vs 88.2 % / 72.8 % at 512).
+# round-1 result (profiles/r01_aes_variants.json): moving the byte-0/3 address
+# arithmetic to IMAD (FSSB_IMAD_ADDR=1) was 10-12 % SLOWER than one PRMT.
 
 
 def build():
@@ -87,6 +90,29 @@ def run(log2n: int):
                           "frac_lds_roof": N * aes / t / (peaks["lds_wavefronts_per_s"] / 5)}
         out[name] = row
         print(name, json.dumps(row), flush=True)
+    # T-table vs bitsliced AES on the PRG expand (2^24 seeds, 3 blocks each)
+    M = 1 << 24
+    seeds = torch.randint(0, 256, (M, 16), dtype=torch.uint8, device=dev)
+    res = torch.empty((M, 48), dtype=torch.uint8, device=dev)
+    ref = torch.empty_like(res)
+    main = _lib.load()
+    for name, fn in (("expand_ttable", main.fss_aes_mmo_expand),
+                     ("expand_bitsliced", main.fss_aes_mmo_expand_bitsliced)):
+        def go(fn=fn, o=(ref if name == "expand_ttable" else res)):
+            assert fn(_dev.ptr(seeds), M, 3, _dev.ptr(o), stream.cuda_stream) == 0
+        go()
+        ts = []
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            go()
+            b.record(stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b) / 1e3)
+        t = sorted(ts)[2]
+        out[name] = {"ms": t * 1e3, "aes_per_s": 3 * M / t}
+        print(name, json.dumps(out[name]), flush=True)
+    assert torch.equal(res, ref)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "aes_variants.json"), "w") as fh:
         json.dump(out, fh, indent=1)

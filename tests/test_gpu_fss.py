@@ -271,3 +271,44 @@ def test_full_size_properties():
     rec = (fss.eval_cmp(0, k0, x).view(torch.int64) + fss.eval_cmp(1, k1, x).view(torch.int64)) & 0xFFFFFFFF
     a = alpha.view(torch.int64)
     assert torch.equal(rec, (x <= a).to(torch.int64))
+
+
+def test_pinned_host_pipeline_matches_device_path():
+    # pinned host x streams through a 2-stream chunked pipeline (H2D / kernel /
+    # D2H overlap); results must equal the single-launch device path bit-exactly
+    N = (1 << 22) + 12345                 # several chunks plus a ragged tail
+    rng = np.random.default_rng(31)
+    alpha, k0, k1 = fss.keygen_cmp(32, rng, N)
+    ea, e0, _ = fss.keygen_eq(32, rng, N)
+    xh = torch.from_numpy(np.random.default_rng(32).integers(0, 1 << 32, N, dtype=np.uint64)
+                          .view(np.int64)).pin_memory().view(torch.uint64)
+    xd = xh.cuda()
+    for party, k in ((0, k0), (1, k1)):
+        h = fss.eval_cmp(party, k, xh)
+        assert not h.is_cuda and h.is_pinned()
+        assert torch.equal(h.view(torch.int64), fss.eval_cmp(party, k, xd).view(torch.int64).cpu())
+    h = fss.eval_eq(0, e0, xh)
+    assert torch.equal(h.view(torch.int64), fss.eval_eq(0, e0, xd).view(torch.int64).cpu())
+    small = xh[:1000].clone().pin_memory()
+    assert torch.equal(fss.eval_cmp(0, k0.take(np.arange(1000)), small).view(torch.int64),
+                       fss.eval_cmp(0, k0, xd)[:1000].view(torch.int64).cpu())
+
+
+def test_bitsliced_expand_matches_ttable():
+    # the bitsliced AES alternative (csrc/aes_bitsliced.cuh) is bit-exact with the
+    # T-table PRG and the reference's PRG vectors
+    import ctypes
+    from paper_2006_04593_b200 import _dev, _lib
+    seeds = torch.from_numpy(np.random.default_rng(41).integers(0, 256, (1 << 16, 16),
+                                                                dtype=np.uint8)).cuda()
+    with open(os.path.join(GOLDEN, "prg_vectors.json")) as fh:
+        vecs = json.load(fh)["vectors"]
+    for i, (s, _) in enumerate(vecs):
+        seeds[i] = torch.from_numpy(np.frombuffer(bytes.fromhex(s), dtype=np.uint8).copy())
+    for blocks in (2, 3):
+        out = torch.empty((seeds.shape[0], 16 * blocks), dtype=torch.uint8, device="cuda")
+        _lib.call("fss_aes_mmo_expand_bitsliced", _dev.ptr(seeds), seeds.shape[0], blocks,
+                  _dev.ptr(out), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        assert torch.equal(out, prg.expand(seeds, blocks))
+    for i, (_, e) in enumerate(vecs):
+        assert out[i].cpu().numpy().tobytes().hex() == e
