@@ -66,6 +66,14 @@ int fss_pcg64_tape(const fss_pcg64_state* st, int n, uint64_t count, int draw_al
                    uint64_t* alpha, uint64_t* alpha0, uint8_t* s0, uint8_t* s1,
                    fss_pcg64_state* st_out, void* stream);
 
+/* RingTensor.random (ring.py:61-65) through numpy's PCG64 Generator:
+ * out[i] = ((integers(0, 2^63)[i] << 1) | integers(0, 2)[i]) mod 2^n_bits,
+ * bit-identical to the reference's draws (both the 64-bit and the buffered
+ * 32-bit stream). st_out as for fss_pcg64_tape. Used for Beaver triples and
+ * share() so the whole dealer runs on device. */
+int fss_pcg64_ring_random(const fss_pcg64_state* st, int n_bits, uint64_t count, uint64_t* out,
+                          fss_pcg64_state* st_out, void* stream);
+
 /* fss._keygen_eq_core (fss.py:173-216). Outputs are level-major with ld=count. */
 int fss_dpf_keygen(int n, uint64_t count, const uint64_t* alpha, const uint64_t* alpha0,
                    const uint8_t* s0, const uint8_t* s1, uint8_t* scw, uint8_t* tcw,

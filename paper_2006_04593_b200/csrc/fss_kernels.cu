@@ -422,6 +422,50 @@ __global__ void pcg64_tape_kernel(TapePlan P, uint64_t* __restrict__ alpha, uint
     }
 }
 
+// RingTensor.random (ring.py:61-65) through numpy's Generator(PCG64):
+//   raw = integers(0, 2^63, uint64)   -> one 64-bit output per element, v >> 1
+//   raw = raw << 1 | integers(0, 2)   -> one 32-bit word per element, w >> 31
+//   raw &= mask(n)
+// (both bounded draws are Lemire with a power-of-two range: no rejection.)
+// The 64-bit part takes outputs [0, count); the 32-bit words follow, with
+// numpy's buffered half-word (has_uint32) served first.
+__global__ void pcg64_ring_kernel(TapePlan P, uint64_t* __restrict__ out) {
+    const uint64_t N = P.count;
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t begin = j * kChunk;
+    if (begin >= N) return;
+    const uint64_t mask = P.n >= 64 ? ~0ULL : ((1ULL << P.n) - 1);
+    const uint64_t h = (uint64_t)P.has_uint32;
+    Pcg base;
+    base.state = ((unsigned __int128)P.state_hi << 64) | P.state_lo;
+    base.inc = ((unsigned __int128)P.inc_hi << 64) | P.inc_lo;
+    Pcg p = pcg_advance(base, begin);    // 64-bit draws: outputs [0, N)
+    Pcg w;                                // 32-bit words: outputs N, N+1, ...
+    uint64_t q = ~0ULL, cur = 0;
+#pragma unroll
+    for (int i = 0; i < kChunk; i++) {
+        const uint64_t k = begin + i;
+        if (k >= N) break;
+        const uint64_t hi = pcg_next(p) & ~1ULL;   // (v >> 1) << 1
+        uint32_t word;
+        if (k < h) {
+            word = P.uinteger;                      // numpy's buffered half-word
+        } else {
+            const uint64_t r = k - h;
+            if (q == ~0ULL) {
+                q = r >> 1;
+                w = pcg_advance(base, N + q);
+                cur = pcg_next(w);
+            } else if ((r >> 1) != q) {
+                q = r >> 1;
+                cur = pcg_next(w);
+            }
+            word = (r & 1) ? (uint32_t)(cur >> 32) : (uint32_t)cur;   // low half first
+        }
+        out[k] = (hi | (uint64_t)(word >> 31)) & mask;
+    }
+}
+
 // ------------------------------------------------------------ runtime glue
 
 constexpr int kOk = FSS_OK, kEinval = FSS_EINVAL, kEcuda = FSS_ECUDA;
@@ -571,6 +615,32 @@ int fss_pcg64_tape(const fss_pcg64_state* st, int n, uint64_t count, int draw_al
     const int bs = 256;
     const uint64_t grid = threads ? (threads + bs - 1) / bs : 1;
     pcg64_tape_kernel<<<(unsigned)grid, bs, 0, (cudaStream_t)stream>>>(P, alpha, alpha0, s0, s1);
+    return check_launch();
+}
+
+int fss_pcg64_ring_random(const fss_pcg64_state* st, int n_bits, uint64_t count, uint64_t* out,
+                          fss_pcg64_state* st_out, void* stream) {
+    if (n_bits < 1 || n_bits > 64) return set_err(kEinval, "ring width out of range%s");
+    TapePlan P;
+    P.state_lo = st->state_lo; P.state_hi = st->state_hi;
+    P.inc_lo = st->inc_lo; P.inc_hi = st->inc_hi;
+    P.n = n_bits; P.count = count; P.draw_alpha = 0;
+    P.has_uint32 = st->has_uint32 ? 1 : 0;
+    P.uinteger = st->uinteger;
+    P.raw64 = count;
+    P.words = count;
+    const uint64_t h = (uint64_t)P.has_uint32;
+    const uint64_t fresh = count > h ? count - h : 0;        // words drawn from new outputs
+    if (st_out) {
+        *st_out = *st;
+        st_out->advance = count + (fresh + 1) / 2;
+        st_out->has_uint32 = count == 0 ? st->has_uint32 : (int)(fresh & 1);
+        st_out->uinteger = 0;  // caller fills from the last raw output when has_uint32
+    }
+    if (count == 0) return kOk;
+    const uint64_t threads = (count + kChunk - 1) / kChunk;
+    const int bs = 256;
+    pcg64_ring_kernel<<<(unsigned)((threads + bs - 1) / bs), bs, 0, (cudaStream_t)stream>>>(P, out);
     return check_launch();
 }
 

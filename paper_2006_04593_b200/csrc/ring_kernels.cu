@@ -96,10 +96,11 @@ __global__ void beaver_kernel(int party, int wb, uint64_t mask, uint64_t count,
 }
 
 int grid_size(uint64_t count) {
-    static int sms = 0;
+    static int sms_of[64] = {0};  // per device; benign race (same value written)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& sms = sms_of[dev & 63];
     if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (!sms) sms = 148;
     }

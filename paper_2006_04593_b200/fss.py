@@ -26,7 +26,7 @@ from typing import Optional
 import numpy as np
 import torch
 
-from . import _dev, _lib, prg
+from . import _dev, _lib, _pcg, prg
 from ._lib import PcgState
 from .ring import ring_mask
 
@@ -219,32 +219,8 @@ def _take_unused(batch, m: int):
 # Randomness tape: numpy's Generator(PCG64) stream reproduced on device
 # ---------------------------------------------------------------------------
 
-_M64 = (1 << 64) - 1
-_M128 = (1 << 128) - 1
-_PCG_MULT = 0x2360ED051FC65DA44385DF649FCCF645
-
-
-def _pcg_jump(state: int, inc: int, delta: int) -> int:
-    acc_mult, acc_plus, cur_mult, cur_plus = 1, 0, _PCG_MULT, inc
-    while delta:
-        if delta & 1:
-            acc_mult = (acc_mult * cur_mult) & _M128
-            acc_plus = (acc_plus * cur_mult + cur_plus) & _M128
-        cur_plus = ((cur_mult + 1) * cur_plus) & _M128
-        cur_mult = (cur_mult * cur_mult) & _M128
-        delta >>= 1
-    return (acc_mult * state + acc_plus) & _M128
-
-
-def _pcg_output(state: int) -> int:
-    hi, lo = state >> 64, state & _M64
-    x, r = hi ^ lo, hi >> 58
-    return ((x >> r) | (x << ((64 - r) & 63))) & _M64
-
-
 def _device_tape_ok(n: int, rng) -> bool:
-    return (1 <= n <= 63 and isinstance(rng, np.random.Generator)
-            and type(rng.bit_generator).__name__ == "PCG64")
+    return 1 <= n <= 63 and _pcg.is_pcg64(rng)
 
 
 def _sample_tape(n: int, rng, count: int, alpha, device):
@@ -260,10 +236,7 @@ def _sample_tape(n: int, rng, count: int, alpha, device):
         # n = 64 (two-call uniform draw, fss.py:48-50) or a non-PCG64 generator:
         # the randomness source itself is host numpy, exactly the reference's calls.
         return _sample_tape_host(n, rng, count, alpha_t if alpha is not None else None, device)
-    st = rng.bit_generator.state
-    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
-    cst = PcgState(s & _M64, s >> 64, inc & _M64, inc >> 64, int(st["has_uint32"]),
-                   int(st["uinteger"]) & 0xFFFFFFFF, 0)
+    cst, st = _pcg.snapshot(rng)
     out_st = PcgState()
     draw_alpha = alpha is None
     a = torch.empty(count, dtype=torch.uint64, device=device) if draw_alpha else alpha_t
@@ -274,16 +247,7 @@ def _sample_tape(n: int, rng, count: int, alpha, device):
         _lib.call("fss_pcg64_tape", cst, n, count, int(draw_alpha),
                   _dev.ptr(a) if draw_alpha else None, _dev.ptr(a0), _dev.ptr(s0), _dev.ptr(s1),
                   out_st, _dev.stream_handle(device))
-    # advance the caller's generator exactly as numpy would have
-    new_state = _pcg_jump(s, inc, int(out_st.advance)) if out_st.advance else s
-    has = int(out_st.has_uint32)
-    if out_st.advance:
-        uint = (_pcg_output(new_state) >> 32) if has else 0
-    else:
-        uint = int(st["uinteger"]) if has else 0
-    rng.bit_generator.state = {"bit_generator": "PCG64",
-                               "state": {"state": new_state, "inc": inc},
-                               "has_uint32": has, "uinteger": uint}
+    _pcg.commit(rng, st, out_st, count > 0)   # advance the caller's rng exactly as numpy would
     return a, a0, s0, s1
 
 

@@ -46,7 +46,7 @@ def test_library_rejects_bad_arguments_without_gpu():
 
 
 def test_pcg_jump_matches_numpy():
-    from paper_2006_04593_b200.fss import _pcg_jump, _pcg_output
+    from paper_2006_04593_b200._pcg import jump as _pcg_jump, output as _pcg_output
     rng = np.random.default_rng(99)
     st = rng.bit_generator.state["state"]
     for delta in (1, 2, 5, 1000, 123456789):
@@ -85,3 +85,43 @@ def test_deserialize_header_errors():
         fss.deserialize_keys(one[:-3])
     assert fss.cmp_key_bits(32) == 6431 and fss.cmp_elem_bytes(32) == 824
     assert fss.eq_elem_bytes(32) == 568
+
+
+def _emulate_ring_random(rng, count, n_bits):
+    """Python restatement of pcg64_ring_kernel + the host commit (_pcg.commit)."""
+    from paper_2006_04593_b200 import _lib, _pcg
+    cst, st = _pcg.snapshot(rng)
+    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    h = int(st["has_uint32"])
+    out = []
+    for k in range(count):
+        hi = _pcg.output(_pcg.jump(s, inc, k + 1)) & ~1
+        if k < h:
+            word = int(st["uinteger"])
+        else:
+            r = k - h
+            v = _pcg.output(_pcg.jump(s, inc, count + r // 2 + 1))
+            word = (v >> 32) if r & 1 else (v & 0xFFFFFFFF)
+        out.append((hi | (word >> 31)) & ((1 << n_bits) - 1))
+    fresh = max(count - h, 0)
+    o = _lib.PcgState()
+    o.advance = count + (fresh + 1) // 2
+    o.has_uint32 = st["has_uint32"] if count == 0 else fresh & 1
+    _pcg.commit(rng, st, o, fresh > 0)
+    return np.array(out, dtype=np.uint64)
+
+
+@pytest.mark.parametrize("pre,count,n_bits", [(0, 7, 32), (1, 7, 32), (0, 8, 64), (3, 1, 16),
+                                              (1, 1, 32), (0, 0, 32), (2, 33, 63)])
+def test_ring_random_stream_matches_numpy(pre, count, n_bits):
+    # RingTensor.random (ring.py:61-65): 64-bit Lemire draws (v >> 1) then buffered
+    # 32-bit draws (w >> 31); the device kernel must follow numpy's stream exactly
+    a, b = np.random.default_rng(9), np.random.default_rng(9)
+    a.integers(0, 2, size=pre, dtype=np.uint64)
+    b.integers(0, 2, size=pre, dtype=np.uint64)
+    raw = a.integers(0, 1 << 63, size=count, dtype=np.uint64)
+    raw = (raw << np.uint64(1)) | a.integers(0, 2, size=count, dtype=np.uint64)
+    mask = np.uint64((1 << n_bits) - 1) if n_bits < 64 else np.uint64(0xFFFFFFFFFFFFFFFF)
+    assert np.array_equal(_emulate_ring_random(b, count, n_bits), raw & mask)
+    assert a.bit_generator.state == b.bit_generator.state
+    assert np.array_equal(a.integers(0, 1 << 40, 5), b.integers(0, 1 << 40, 5))

@@ -312,3 +312,20 @@ def test_bitsliced_expand_matches_ttable():
         assert torch.equal(out, prg.expand(seeds, blocks))
     for i, (_, e) in enumerate(vecs):
         assert out[i].cpu().numpy().tobytes().hex() == e
+
+
+@pytest.mark.parametrize("pre,shape,n_bits", [(0, (1000,), 32), (1, (7, 33), 32), (3, (5,), 64),
+                                              (0, (1 << 20,), 32), (2, (64, 3, 5), 16), (1, (1,), 63),
+                                              (0, (), 32)])
+def test_ring_random_on_device_matches_numpy(pre, shape, n_bits):
+    from paper_2006_04593_b200.ring import RingTensor
+    a, b = np.random.default_rng(12), np.random.default_rng(12)
+    a.integers(0, 2, size=pre, dtype=np.uint64)
+    b.integers(0, 2, size=pre, dtype=np.uint64)
+    raw = a.integers(0, 1 << 63, size=shape, dtype=np.uint64)
+    raw = (raw << np.uint64(1)) | a.integers(0, 2, size=shape, dtype=np.uint64)
+    mask = np.uint64((1 << n_bits) - 1) if n_bits < 64 else np.uint64(0xFFFFFFFFFFFFFFFF)
+    t = RingTensor.random(shape, n_bits, b)
+    assert t.data.is_cuda and tuple(t.shape) == tuple(shape)
+    assert np.array_equal(t.numpy(), raw & mask)
+    assert a.bit_generator.state == b.bit_generator.state
