@@ -96,6 +96,19 @@ int fss_dcf_eval(int party, int n, int out_bits, uint64_t count, uint64_t ld, co
                  const uint64_t* leaf_cw, const uint64_t* x, uint64_t* out, uint64_t* levels,
                  void* stream);
 
+/* The two evaluations fused with the opening of the single online message of
+ * sign_protocol / eq_protocol (fss.py:444-491 -> sharing.mask_and_reveal,
+ * sharing.py:214-230): x[e] = (m_own[e] + m_peer[e]) mod 2^n, where m_own /
+ * m_peer are the two parties' wire-packed masked inputs (width
+ * fss_wire_bytes(n)). Saves the separate open kernel and the x round trip. */
+int fss_dpf_eval_masked(int party, int n, uint64_t count, uint64_t ld, const uint8_t* seed0,
+                        const uint8_t* scw, const uint8_t* tcw, const uint64_t* cw_final,
+                        const void* m_own, const void* m_peer, uint64_t* out, void* stream);
+int fss_dcf_eval_masked(int party, int n, int out_bits, uint64_t count, uint64_t ld,
+                        const uint8_t* seed0, const uint8_t* scw, const uint8_t* tcw,
+                        const uint64_t* sigma_cw, const uint64_t* leaf_cw, const void* m_own,
+                        const void* m_peer, uint64_t* out, void* stream);
+
 /* ARNK per-party payloads (LAYOUT.md:48-71; fss._pack_eq/_pack_cmp fss.py:540-583,
  * _unpack_eq/_unpack_cmp fss.py:553-602). kind 0 = equality, 1 = comparison.
  * payload is count * fss_arnk_elem_bytes(kind, n) bytes, element-major.

@@ -88,6 +88,16 @@ expand_kernel(const uint8_t* __restrict__ seeds, uint64_t count, int blocks, uin
     }
 }
 
+// Public input of element e: x[e], or -- fused with the one online round of
+// sign/eq_protocol (sharing.mask_and_reveal, sharing.py:214-230) -- the opening
+// m_own[e] + m_peer[e] of the two parties' wire-packed masked messages.
+__device__ __forceinline__ uint64_t load_x(const uint64_t* __restrict__ x, const void* __restrict__ m_own,
+                                           const void* __restrict__ m_peer, int n, uint64_t e) {
+    if (x) return x[e];
+    const int wb = fssb::wire_bytes(n);
+    return fssb::wire_get(wb, m_own, e) + fssb::wire_get(wb, m_peer, e);
+}
+
 // ---------------------------------------------------------------- DPF eval
 // fss.eval_eq (fss.py:357-377): t0 = party, per level expand, correct with
 // scw/tcw when t, descend to child x_i (MSB first); out = t*cw_final + s2r(s).
@@ -95,6 +105,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 dpf_eval_kernel(int party, int n, uint64_t count, uint64_t ld, const uint8_t* __restrict__ seed0,
                 const uint8_t* __restrict__ scw, const uint8_t* __restrict__ tcw,
                 const uint64_t* __restrict__ cw_final, const uint64_t* __restrict__ x,
+                const void* __restrict__ m_own, const void* __restrict__ m_peer,
                 uint64_t* __restrict__ out) {
     extern __shared__ uint32_t tab[];
     fssb::fill_tables(tab);
@@ -105,7 +116,7 @@ dpf_eval_kernel(int party, int n, uint64_t count, uint64_t ld, const uint8_t* __
          e += (uint64_t)gridDim.x * blockDim.x) {
         U4 s = ld16(seed0 + 16 * e);
         uint32_t t = party;
-        const uint64_t xe = x[e] & mask;
+        const uint64_t xe = load_x(x, m_own, m_peer, n, e) & mask;
 #if FSSB_PREFETCH_DPF
         // software pipeline: level i+1's correction words load during level i's AES
         U4 cw = ld16(scw + 16 * e);
@@ -147,6 +158,7 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
                 const uint8_t* __restrict__ seed0, const uint8_t* __restrict__ scw,
                 const uint8_t* __restrict__ tcw, const uint64_t* __restrict__ sigma_cw,
                 const uint64_t* __restrict__ leaf_cw, const uint64_t* __restrict__ x,
+                const void* __restrict__ m_own, const void* __restrict__ m_peer,
                 uint64_t* __restrict__ out, uint64_t* __restrict__ levels) {
     extern __shared__ uint32_t tab[];
     fssb::fill_tables(tab);
@@ -159,7 +171,7 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
         U4 s = ld16(seed0 + 16 * e);
         uint32_t t = party;
         uint64_t acc = 0;
-        const uint64_t xe = x[e] & nmask;
+        const uint64_t xe = load_x(x, m_own, m_peer, n, e) & nmask;
 #if FSSB_PREFETCH_DCF
         U4 cw = ld16(scw + 16 * e);
         uint32_t f = __ldg(tcw + e);
@@ -525,32 +537,73 @@ int fss_aes_mmo_expand(const uint8_t* seeds, uint64_t count, int out_blocks, uin
     return check_launch();
 }
 
-int fss_dpf_eval(int party, int n, uint64_t count, uint64_t ld, const uint8_t* seed0,
-                 const uint8_t* scw, const uint8_t* tcw, const uint64_t* cw_final, const uint64_t* x,
-                 uint64_t* out, void* stream) {
+}  // extern "C"
+
+namespace {
+
+int launch_dpf_eval(int party, int n, uint64_t count, uint64_t ld, const uint8_t* seed0,
+                    const uint8_t* scw, const uint8_t* tcw, const uint64_t* cw_final,
+                    const uint64_t* x, const void* m_own, const void* m_peer, uint64_t* out,
+                    void* stream) {
     if (party != 0 && party != 1) return set_err(kEinval, "party must be 0 or 1%s");
     if (n < 1 || n > 64) return set_err(kEinval, "n out of range%s");
     if (count == 0) return kOk;
+    if (!x && (!m_own || !m_peer)) return set_err(kEinval, "need x or both masked messages%s");
     int sms;
     if (int rc = prep_launch(dpf_eval_kernel, &sms)) return rc;
     dpf_eval_kernel<<<grid_for(count, sms, kThreads), kThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
-        party, n, count, ld, seed0, scw, tcw, cw_final, x, out);
+        party, n, count, ld, seed0, scw, tcw, cw_final, x, m_own, m_peer, out);
     return check_launch();
+}
+
+int launch_dcf_eval(int party, int n, int out_bits, uint64_t count, uint64_t ld, const uint8_t* seed0,
+                    const uint8_t* scw, const uint8_t* tcw, const uint64_t* sigma_cw,
+                    const uint64_t* leaf_cw, const uint64_t* x, const void* m_own, const void* m_peer,
+                    uint64_t* out, uint64_t* levels, void* stream) {
+    if (party != 0 && party != 1) return set_err(kEinval, "party must be 0 or 1%s");
+    if (n < 1 || n > 63 || out_bits < n || out_bits > 63)
+        return set_err(kEinval, "need 1 <= n <= out_bits <= 63%s");
+    if (count == 0) return kOk;
+    if (!x && (!m_own || !m_peer)) return set_err(kEinval, "need x or both masked messages%s");
+    int sms;
+    if (int rc = prep_launch(dcf_eval_kernel, &sms)) return rc;
+    dcf_eval_kernel<<<grid_for(count, sms, kThreads), kThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+        party, n, out_bits, count, ld, seed0, scw, tcw, sigma_cw, leaf_cw, x, m_own, m_peer, out, levels);
+    return check_launch();
+}
+
+}  // namespace
+
+extern "C" {
+
+int fss_dpf_eval(int party, int n, uint64_t count, uint64_t ld, const uint8_t* seed0,
+                 const uint8_t* scw, const uint8_t* tcw, const uint64_t* cw_final, const uint64_t* x,
+                 uint64_t* out, void* stream) {
+    return launch_dpf_eval(party, n, count, ld, seed0, scw, tcw, cw_final, x, nullptr, nullptr, out,
+                           stream);
+}
+
+int fss_dpf_eval_masked(int party, int n, uint64_t count, uint64_t ld, const uint8_t* seed0,
+                        const uint8_t* scw, const uint8_t* tcw, const uint64_t* cw_final,
+                        const void* m_own, const void* m_peer, uint64_t* out, void* stream) {
+    return launch_dpf_eval(party, n, count, ld, seed0, scw, tcw, cw_final, nullptr, m_own, m_peer, out,
+                           stream);
 }
 
 int fss_dcf_eval(int party, int n, int out_bits, uint64_t count, uint64_t ld, const uint8_t* seed0,
                  const uint8_t* scw, const uint8_t* tcw, const uint64_t* sigma_cw,
                  const uint64_t* leaf_cw, const uint64_t* x, uint64_t* out, uint64_t* levels,
                  void* stream) {
-    if (party != 0 && party != 1) return set_err(kEinval, "party must be 0 or 1%s");
-    if (n < 1 || n > 63 || out_bits < n || out_bits > 63)
-        return set_err(kEinval, "need 1 <= n <= out_bits <= 63%s");
-    if (count == 0) return kOk;
-    int sms;
-    if (int rc = prep_launch(dcf_eval_kernel, &sms)) return rc;
-    dcf_eval_kernel<<<grid_for(count, sms, kThreads), kThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
-        party, n, out_bits, count, ld, seed0, scw, tcw, sigma_cw, leaf_cw, x, out, levels);
-    return check_launch();
+    return launch_dcf_eval(party, n, out_bits, count, ld, seed0, scw, tcw, sigma_cw, leaf_cw, x, nullptr,
+                           nullptr, out, levels, stream);
+}
+
+int fss_dcf_eval_masked(int party, int n, int out_bits, uint64_t count, uint64_t ld,
+                        const uint8_t* seed0, const uint8_t* scw, const uint8_t* tcw,
+                        const uint64_t* sigma_cw, const uint64_t* leaf_cw, const void* m_own,
+                        const void* m_peer, uint64_t* out, void* stream) {
+    return launch_dcf_eval(party, n, out_bits, count, ld, seed0, scw, tcw, sigma_cw, leaf_cw, nullptr,
+                           m_own, m_peer, out, nullptr, stream);
 }
 
 int fss_dpf_keygen(int n, uint64_t count, const uint64_t* alpha, const uint64_t* alpha0,

@@ -32,19 +32,7 @@ __global__ void ring_kernel(int op, uint64_t mask, uint64_t count, const uint64_
 
 // Wire format of the share layer (sharing.py:191-207 pack_ring/_wire_dtype):
 // ring values travel at the smallest power-of-two byte width covering n_bits.
-template <typename W>
-__device__ __forceinline__ uint64_t wire_ld(const void* p, uint64_t i) {
-    return (uint64_t)reinterpret_cast<const W*>(p)[i];
-}
-
-__device__ __forceinline__ uint64_t wire_get(int wb, const void* p, uint64_t i) {
-    switch (wb) {
-        case 1: return wire_ld<uint8_t>(p, i);
-        case 2: return wire_ld<uint16_t>(p, i);
-        case 4: return wire_ld<uint32_t>(p, i);
-        default: return wire_ld<uint64_t>(p, i);
-    }
-}
+using fssb::wire_get;
 
 __device__ __forceinline__ void wire_put(int wb, void* p, uint64_t i, uint64_t v) {
     switch (wb) {
@@ -130,7 +118,7 @@ int fss_ring_op(int op, int n_bits, uint64_t count, const uint64_t* a, const uin
 
 int fss_wire_bytes(int n_bits) {
     if (n_bits < 1 || n_bits > 64) return 0;
-    return n_bits <= 8 ? 1 : n_bits <= 16 ? 2 : n_bits <= 32 ? 4 : 8;
+    return fssb::wire_bytes(n_bits);
 }
 
 int fss_wire_pack(int op, int n_bits, uint64_t count, const uint64_t* a, const uint64_t* b,

@@ -511,10 +511,52 @@ def set_sign_probe(probe):
     _sign_probe = probe
 
 
+def _masked_round(session, y, alpha_share, n: int, op: str):
+    """The one online round of mask_and_reveal (sharing.py:214-230) up to the
+    opening: returns this party's wire-packed m_j = y_j + alpha_j and the
+    peer's. The opening x = m_0 + m_1 happens inside the evaluation kernel."""
+    from .runtime import FRAME_MASKED
+    from .sharing import _flat_u64, _pack, _peer_wire
+
+    masked = _pack(0, _flat_u64(y.values), _flat_u64(alpha_share), n)
+    peer = session.exchange(op, FRAME_MASKED, masked, elements=masked.numel())
+    return masked, _peer_wire(peer, n, masked.numel(), masked.device)
+
+
+def _eval_cmp_masked(party: int, k: CmpKeyBatch, m_own, m_peer) -> torch.Tensor:
+    k.validate()
+    dev = k.device
+    ld = _eval_operands(k, ("tcw", "sigma_cw", "leaf_cw"))
+    seed0 = k.seed0.contiguous()
+    out = torch.empty(k.count, dtype=torch.uint64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.call("fss_dcf_eval_masked", int(party), k.n_bits, int(k.out_bits), k.count, ld,
+                  _dev.ptr(seed0), _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(k.sigma_cw),
+                  _dev.ptr(k.leaf_cw), _dev.ptr(m_own), _dev.ptr(m_peer), _dev.ptr(out),
+                  _dev.stream_handle(dev))
+    return out
+
+
+def _eval_eq_masked(party: int, k: EqKeyBatch, m_own, m_peer) -> torch.Tensor:
+    k.validate()
+    dev = k.device
+    ld = _eval_operands(k, ("tcw",))
+    seed0, cw_final = k.seed0.contiguous(), k.cw_final.contiguous()
+    out = torch.empty(k.count, dtype=torch.uint64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.call("fss_dpf_eval_masked", int(party), k.n_bits, k.count, ld, _dev.ptr(seed0),
+                  _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(cw_final), _dev.ptr(m_own),
+                  _dev.ptr(m_peer), _dev.ptr(out), _dev.stream_handle(dev))
+    return out
+
+
 def sign_protocol(session, y, keys: CmpKeyBatch):
-    """Shares of 1[y <= 0] for an additively shared y. One online round (fss.py:444-473)."""
+    """Shares of 1[y <= 0] for an additively shared y. One online round (fss.py:444-473).
+
+    The masked message m_j = y_j + alpha_j is wire-packed on device, exchanged,
+    and opened inside the DCF evaluation kernel (fss_dcf_eval_masked)."""
     from .ring import RingTensor
-    from .sharing import AdditiveShare, mask_and_reveal
+    from .sharing import AdditiveShare
     from . import ring_ops
 
     m = y.values.size
@@ -527,8 +569,8 @@ def sign_protocol(session, y, keys: CmpKeyBatch):
         # Narrow-domain keys: mask and reveal only the low domain bits.
         y = AdditiveShare(y.party, RingTensor(ring_ops.mask(y.values.data, keys.n_bits),
                                               keys.n_bits, _trusted=True), 0)
-    x = mask_and_reveal(session, y, ks.alpha_share.reshape(y.values.shape), op="comparison")
-    out = eval_cmp(y.party, ks, x.data.reshape(-1))
+    m_own, m_peer = _masked_round(session, y, ks.alpha_share, keys.n_bits, "comparison")
+    out = _eval_cmp_masked(y.party, ks, m_own, m_peer)
     if _sign_probe is not None:
         _sign_probe(y.party, y.values.data.reshape(-1), out, ks.n_bits, ks.out_bits)
     values = RingTensor(out.reshape(y.values.shape), ks.out_bits, _trusted=True)
@@ -538,7 +580,7 @@ def sign_protocol(session, y, keys: CmpKeyBatch):
 def eq_protocol(session, y, keys: EqKeyBatch):
     """Shares of 1[y == 0] for an additively shared y. One online round, exact (fss.py:476-491)."""
     from .ring import RingTensor
-    from .sharing import AdditiveShare, mask_and_reveal
+    from .sharing import AdditiveShare
 
     m = y.values.size
     if keys.n_bits != y.values.n_bits:
@@ -546,8 +588,8 @@ def eq_protocol(session, y, keys: EqKeyBatch):
     if keys.party != y.party:
         raise ValueError("key batch belongs to the other party")
     ks = keys.take_unused(m)
-    x = mask_and_reveal(session, y, ks.alpha_share.reshape(y.values.shape), op="equality")
-    out = eval_eq(y.party, ks, x.data.reshape(-1))
+    m_own, m_peer = _masked_round(session, y, ks.alpha_share, keys.n_bits, "equality")
+    out = _eval_eq_masked(y.party, ks, m_own, m_peer)
     values = RingTensor(out.reshape(y.values.shape), y.values.n_bits, _trusted=True)
     return AdditiveShare(y.party, values, precision=0)
 
