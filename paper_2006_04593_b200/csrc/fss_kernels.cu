@@ -18,6 +18,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <type_traits>
+
 #include "../../include/ariann_fss.h"
 #include "aes_ttable.cuh"
 #include "common.cuh"
@@ -40,6 +42,9 @@ namespace {
 #undef FSSB_PREFETCH_DPF
 #define FSSB_PREFETCH_DCF FSSB_PREFETCH
 #define FSSB_PREFETCH_DPF FSSB_PREFETCH
+#endif
+#ifndef FSSB_W32
+#define FSSB_W32 1
 #endif
 #ifndef FSSB_THREADS
 #define FSSB_THREADS 1024
@@ -153,6 +158,13 @@ dpf_eval_kernel(int party, int n, uint64_t count, uint64_t ld, const uint8_t* __
 // ---------------------------------------------------------------- DCF eval
 // fss.eval_cmp (fss.py:380-426). Per level: child block (key k1/k2 by x_i) and
 // the sigma/tau block (k3, lane x_i). out_i = tau*leaf[i] + sigma (mod 2^w).
+//
+// Ring arithmetic is mod 2^w, so the running sum is reduced once at the end
+// (per level only when the per-level outputs are requested). W32: for
+// out_bits <= 32 (hence n <= 32) sigma, leaf and the sum live in 32-bit
+// registers and only the low words of sigma_cw / leaf_cw are read (values
+// < 2^w, little-endian), which removes the 64-bit glue from the ALU pipe.
+template <bool W32>
 __global__ void __launch_bounds__(kThreads, 1)
 dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
                 const uint8_t* __restrict__ seed0, const uint8_t* __restrict__ scw,
@@ -160,49 +172,56 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
                 const uint64_t* __restrict__ leaf_cw, const uint64_t* __restrict__ x,
                 const void* __restrict__ m_own, const void* __restrict__ m_peer,
                 uint64_t* __restrict__ out, uint64_t* __restrict__ levels) {
+    using W = typename std::conditional<W32, uint32_t, uint64_t>::type;
     extern __shared__ uint32_t tab[];
     fssb::fill_tables(tab);
     __syncthreads();
     const fssb::Tab tb = fssb::make_tab(tab);
     const uint64_t nmask = ring_mask(n);
     const uint64_t mask = ring_mask(out_bits);
+    const W* __restrict__ sig_w = reinterpret_cast<const W*>(sigma_cw);
+    const W* __restrict__ leaf_w = reinterpret_cast<const W*>(leaf_cw);
+    constexpr int kStride = W32 ? 2 : 1;   // W-words per u64 element
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
          e += (uint64_t)gridDim.x * blockDim.x) {
         U4 s = ld16(seed0 + 16 * e);
         uint32_t t = party;
-        uint64_t acc = 0;
+        W acc = 0;
         const uint64_t xe = load_x(x, m_own, m_peer, n, e) & nmask;
 #if FSSB_PREFETCH_DCF
         U4 cw = ld16(scw + 16 * e);
         uint32_t f = __ldg(tcw + e);
-        uint64_t sig = __ldg(sigma_cw + e);
-        uint64_t leaf = __ldg(leaf_cw + e);
+        W sig = __ldg(sig_w + kStride * e);
+        W leaf = __ldg(leaf_w + kStride * e);
 #endif
         for (int i = 0; i < n; i++) {
 #if FSSB_PREFETCH_DCF
             const uint64_t offn = (uint64_t)(i + 1 < n ? i + 1 : i) * ld + e;
             const U4 cw_next = ld16(scw + 16 * offn);
             const uint32_t f_next = __ldg(tcw + offn);
-            const uint64_t sig_next = __ldg(sigma_cw + offn);
-            const uint64_t leaf_next = __ldg(leaf_cw + offn);
+            const W sig_next = __ldg(sig_w + kStride * offn);
+            const W leaf_next = __ldg(leaf_w + kStride * offn);
 #else
             const uint64_t off = (uint64_t)i * ld + e;
             const U4 cw = ld16(scw + 16 * off);
             const uint32_t f = __ldg(tcw + off);
-            const uint64_t sig = __ldg(sigma_cw + off);
-            const uint64_t leaf = __ldg(leaf_cw + off);
+            const W sig = __ldg(sig_w + kStride * off);
+            const W leaf = __ldg(leaf_w + kStride * off);
 #endif
             const uint32_t xb = (uint32_t)(xe >> (n - 1 - i)) & 1u;
             const U4 a = fssb::mmo<0, true>(tb, s, 0u - xb);
             const U4 g = fssb::mmo<2, false>(tb, s, 0);
             const uint32_t tm = 0u - t;
             // sigma/tau lane x_i of the third block (slice_cmp, prg.py:99-119)
-            const uint64_t lane = xb ? hi64(g) : lo64(g);
-            const uint32_t tau = ((uint32_t)(lane >> 63) ^ (t & (f >> (2 + xb)))) & 1u;
-            const uint64_t sigma = (lane & mask) ^ (sig & (0ULL - (uint64_t)t));
-            const uint64_t oi = (((uint64_t)tau * leaf) + sigma) & mask;
-            acc = (acc + oi) & mask;
-            if (levels) levels[(uint64_t)i * count + e] = party ? ((0 - oi) & mask) : oi;
+            const uint32_t lane_hi = xb ? g.w : g.y;
+            W lane;
+            if (W32) lane = (W)(xb ? g.z : g.x);
+            else lane = (W)(xb ? hi64(g) : lo64(g));
+            const uint32_t tau = ((lane_hi >> 31) ^ (t & (f >> (2 + xb)))) & 1u;
+            const W sigma = lane ^ (sig & (W)(0 - (W)t));
+            const W oi = (leaf & (W)(0 - (W)tau)) + sigma;
+            acc += oi;
+            if (levels) levels[(uint64_t)i * count + e] = (party ? (0 - (uint64_t)oi) : (uint64_t)oi) & mask;
             s = xor4(a, and4(cw, tm));
             const uint32_t tn = ((a.w >> 31) ^ (t & (f >> xb))) & 1u;
             s.w &= 0x7FFFFFFFu;
@@ -215,10 +234,11 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
 #endif
         }
         const uint64_t off = (uint64_t)n * ld + e;
-        const uint64_t last = (((uint64_t)t * __ldg(leaf_cw + off)) + lo64(s)) & mask;
-        acc = (acc + last) & mask;
-        if (levels) levels[(uint64_t)n * count + e] = party ? ((0 - last) & mask) : last;
-        out[e] = party ? ((0 - acc) & mask) : acc;
+        const W lo = W32 ? (W)s.x : (W)lo64(s);
+        const W last = (__ldg(leaf_w + kStride * off) & (W)(0 - (W)t)) + lo;
+        acc += last;
+        if (levels) levels[(uint64_t)n * count + e] = (party ? (0 - (uint64_t)last) : (uint64_t)last) & mask;
+        out[e] = (party ? (0 - (uint64_t)acc) : (uint64_t)acc) & mask;
     }
 }
 
@@ -512,6 +532,21 @@ int grid_for(uint64_t count, int sms, int threads) {
     return (int)(need < (uint64_t)sms ? (need ? need : 1) : sms);
 }
 
+// Eval launch shape: one CTA per SM (the tables fill 128 KiB of shared
+// memory). Batches too small to give every SM kThreads threads are spread
+// over all SMs with fewer threads each instead of leaving SMs idle.
+int eval_grid(uint64_t count, int sms, int* threads) {
+    const uint64_t per_sm = (count + sms - 1) / sms;
+    if (per_sm >= (uint64_t)kThreads) {
+        *threads = kThreads;
+        return sms;
+    }
+    *threads = (int)(((per_sm + 31) / 32) * 32);
+    if (*threads < 32) *threads = 32;
+    const uint64_t grid = (count + *threads - 1) / *threads;
+    return (int)(grid < (uint64_t)sms ? (grid ? grid : 1) : sms);
+}
+
 int check_launch() {
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) return set_err(kEcuda, "kernel launch: %s", cudaGetErrorString(err));
@@ -551,7 +586,9 @@ int launch_dpf_eval(int party, int n, uint64_t count, uint64_t ld, const uint8_t
     if (!x && (!m_own || !m_peer)) return set_err(kEinval, "need x or both masked messages%s");
     int sms;
     if (int rc = prep_launch(dpf_eval_kernel, &sms)) return rc;
-    dpf_eval_kernel<<<grid_for(count, sms, kThreads), kThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+    int threads;
+    const int grid = eval_grid(count, sms, &threads);
+    dpf_eval_kernel<<<grid, threads, fssb::kTableBytes, (cudaStream_t)stream>>>(
         party, n, count, ld, seed0, scw, tcw, cw_final, x, m_own, m_peer, out);
     return check_launch();
 }
@@ -566,8 +603,12 @@ int launch_dcf_eval(int party, int n, int out_bits, uint64_t count, uint64_t ld,
     if (count == 0) return kOk;
     if (!x && (!m_own || !m_peer)) return set_err(kEinval, "need x or both masked messages%s");
     int sms;
-    if (int rc = prep_launch(dcf_eval_kernel, &sms)) return rc;
-    dcf_eval_kernel<<<grid_for(count, sms, kThreads), kThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+    const bool w32 = FSSB_W32 && out_bits <= 32;
+    auto kern = w32 ? dcf_eval_kernel<true> : dcf_eval_kernel<false>;
+    if (int rc = prep_launch(kern, &sms)) return rc;
+    int threads;
+    const int grid = eval_grid(count, sms, &threads);
+    kern<<<grid, threads, fssb::kTableBytes, (cudaStream_t)stream>>>(
         party, n, out_bits, count, ld, seed0, scw, tcw, sigma_cw, leaf_cw, x, m_own, m_peer, out, levels);
     return check_launch();
 }

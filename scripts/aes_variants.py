@@ -19,7 +19,7 @@ VDIR = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = {
     "default": [],
-    "no_lop3_combine": ["FSSB_LOP3_COMBINE=0"],
+    "w64": ["FSSB_W32=0"],
 }
 # round-1 sweep b (profiles/r01_aes_variants_b.json): 512/640/768/1024 threads
 # x prefetch; more resident warps win (1024: DCF 92.9 %, DPF 85.5 % of the
@@ -125,3 +125,5 @@ if __name__ == "__main__":
     else:
         n = int(sys.argv[sys.argv.index("--log2n") + 1]) if "--log2n" in sys.argv else 22
         run(n)
+        if "--small" in sys.argv:
+            run(16)
