@@ -203,15 +203,33 @@ class CmpKeyBatch:
 
 
 def _take_unused(batch, m: int):
-    """Single-use key hand-out (fss.py:157-166)."""
-    free = np.flatnonzero(~batch.consumed)
+    """Single-use key hand-out (fss.py:157-166): the first m unconsumed keys.
+
+    Keys are normally spent front to back. ``_free_hint`` h keeps the invariant
+    consumed[:h] all True (consuming more keys never breaks it), so when
+    consumed[h : h+m] are all free they ARE the first m free keys and go out as
+    one contiguous zero-copy slice in O(m); otherwise the full scan is used."""
+    consumed = batch.consumed
+    count = consumed.shape[0]
+    h = min(getattr(batch, "_free_hint", 0), count)
+    if h and not consumed[h - 1]:   # mask was replaced / edited: drop the hint
+        h = 0
+    if m == 0 or (h + m <= count and not consumed[h:h + m].any()):
+        out = batch.take(slice(h, h + m))
+        consumed[h:h + m] = True
+        batch._free_hint = h + m
+        out.consumed[:] = True
+        return out
+    free = np.flatnonzero(~consumed)
     if free.size < m:
         raise KeyExhaustedError(
             f"requested {m} keys but only {free.size} unconsumed remain (single-use)")
     idx = free[:m]
     out = batch.take(idx)
-    batch.consumed[idx] = True
+    consumed[idx] = True
     out.consumed[:] = True  # the view itself is spent once handed out
+    # everything before the next free key is now consumed
+    batch._free_hint = int(free[m]) if free.size > m else count
     return out
 
 
@@ -409,7 +427,7 @@ def _eval_operands(k, names):
 # chunks on two CUDA streams, so the H2D copy of x, the evaluation kernel and
 # the D2H copy of the shares of consecutive chunks overlap.
 PIPELINE_MIN = 1 << 21
-PIPELINE_CHUNK = 1 << 21
+PIPELINE_CHUNK = 1 << 20
 
 
 def _run_eval(launch, xt, host, count: int, dev):

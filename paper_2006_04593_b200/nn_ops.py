@@ -77,9 +77,12 @@ def _pairwise_diffs(data: torch.Tensor, m: int) -> torch.Tensor:
     """[..., j, i] = x_i - x_j with the diagonal removed, grouped by j
     (nn_ops.py:111-114): (..., m*(m-1))."""
     v = _dev.as_i64(data)
-    diffs = v[..., None, :] - v[..., :, None]
-    off = ~torch.eye(m, dtype=torch.bool, device=v.device)
-    return _dev.as_u64(diffs[..., off])
+    diffs = (v[..., None, :] - v[..., :, None]).reshape(*v.shape[:-1], m * m)
+    # off-diagonal positions in row-major (j, i) order; index_select keeps the
+    # whole step on device (boolean-mask indexing would sync on nonzero())
+    off = torch.tensor([j * m + i for j in range(m) for i in range(m) if i != j],
+                       dtype=torch.int64, device=v.device)
+    return _dev.as_u64(diffs.index_select(-1, off))
 
 
 def argmax(session, x: AdditiveShare, prep: ArgmaxPrep) -> AdditiveShare:

@@ -38,7 +38,7 @@ for _ in range(5):
     fss.eval_cmp(1, k1, xd)
 torch.cuda.synchronize()
 out["device_only_cmp_per_s"] = 5 * N / (time.perf_counter() - t0)
-for chunk in (1 << 19, 1 << 20, 1 << 21, 1 << 22, 1 << 23):
+for chunk in (1 << 20, 1 << 21, 1 << 22, 1 << 20, 1 << 21, 1 << 22, 1 << 19, 1 << 20):
     fss.PIPELINE_CHUNK = chunk
     fss.eval_cmp(0, k0, xh)
     t0 = time.perf_counter()
@@ -47,5 +47,5 @@ for chunk in (1 << 19, 1 << 20, 1 << 21, 1 << 22, 1 << 23):
         r1 = fss.eval_cmp(1, k1, xh)
     dt = time.perf_counter() - t0
     assert bool(((r0.view(torch.int64) + r1.view(torch.int64)) & 0xFFFFFFFF == 1).all())
-    out[f"pinned_chunk_2^{chunk.bit_length() - 1}_cmp_per_s"] = 5 * N / dt
+    out.setdefault(f"pinned_chunk_2^{chunk.bit_length() - 1}_cmp_per_s", []).append(5 * N / dt)
 print(json.dumps(out, indent=1))

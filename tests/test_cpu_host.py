@@ -125,3 +125,41 @@ def test_ring_random_stream_matches_numpy(pre, count, n_bits):
     assert np.array_equal(_emulate_ring_random(b, count, n_bits), raw & mask)
     assert a.bit_generator.state == b.bit_generator.state
     assert np.array_equal(a.integers(0, 1 << 40, 5), b.integers(0, 1 << 40, 5))
+
+
+def test_take_unused_fast_path_and_fallback():
+    # the hint-based fast path must hand out exactly the first m free keys
+    from paper_2006_04593_b200 import fss
+
+    class Fake:
+        def __init__(self, n):
+            self.consumed = np.zeros(n, dtype=bool)
+            self.taken = []
+
+        def take(self, idx):
+            self.taken.append(idx)
+
+            class V:
+                consumed = np.zeros(1, dtype=bool)
+            return V()
+    rng = np.random.default_rng(0)
+    for trial in range(200):
+        f = Fake(50)
+        ref = np.zeros(50, dtype=bool)
+        for _ in range(8):
+            if rng.random() < 0.3:   # an audit consumes random keys
+                pick = rng.integers(0, 50, 3)
+                f.consumed[pick] = True
+                ref[pick] = True
+            m = int(rng.integers(0, 9))
+            free = np.flatnonzero(~ref)
+            if free.size < m:
+                with pytest.raises(fss.KeyExhaustedError):
+                    fss._take_unused(f, m)
+                continue
+            fss._take_unused(f, m)
+            got = f.taken[-1]
+            got = np.arange(got.start, got.stop) if isinstance(got, slice) else np.asarray(got)
+            assert np.array_equal(got, free[:m])
+            ref[free[:m]] = True
+            assert np.array_equal(f.consumed, ref)
