@@ -246,6 +246,30 @@ def measure_secondary(dev, args):
     return out
 
 
+def measure_exchange(dev, xdev, rank, ws, N, barrier, max_over_ranks):
+    """The one online message of a comparison when the two parties sit on
+    different GPUs: rank r (party r % 2) swaps its wire-packed masked inputs
+    (N x u32 at n = 32) with rank r ^ 1 through runtime.DistTransport (NCCL
+    point-to-point over NVLink / NVSwitch). Max over ranks, 5 exchanges."""
+    import torch
+
+    from paper_2006_04593_b200 import runtime
+
+    sess = runtime.Session(rank % 2, runtime.DistTransport(rank ^ 1, device=xdev))
+    msg = torch.full((N,), rank, dtype=torch.int32, device=dev)   # u32 wire words
+    peer = sess.exchange("comparison", runtime.FRAME_MASKED, msg, N)
+    assert int(peer[0]) == (rank ^ 1)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(5):
+        sess.exchange("comparison", runtime.FRAME_MASKED, msg, N)
+    torch.cuda.synchronize()
+    t = max_over_ranks((time.perf_counter() - t0) / 5)
+    return {"bytes_each_way_per_rank": 4 * N, "ms": t * 1e3, "GBps_each_way": 4 * N / t / 1e9,
+            "pairs": ws // 2, "note": "wall clock incl. the 24-byte frame header round trip"}
+
+
 def run_ours(args, ws, rank, local):
     import numpy as np
     import torch
@@ -254,10 +278,21 @@ def run_ours(args, ws, rank, local):
     from paper_2006_04593_b200 import _lib, fss
 
     _lib.load()  # fail loudly without the CUDA library
+    # Test-only: FSS_BENCH_SAME_GPU=1 puts every rank on cuda:0 over gloo so the
+    # N>1 code path can be exercised on a single-GPU box (numbers meaningless).
+    same_gpu = os.environ.get("FSS_BENCH_SAME_GPU") == "1"
+    if same_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        import datetime
+        timeout = datetime.timedelta(minutes=10)
+        if same_gpu:
+            dist.init_process_group("gloo", timeout=timeout)
+        else:
+            dist.init_process_group("nccl", device_id=dev, timeout=timeout)
+    xdev = torch.device("cpu") if same_gpu else dev     # device for collectives
     N = 1 << args.log2n
 
     def barrier():
@@ -267,7 +302,7 @@ def run_ours(args, ws, rank, local):
     def max_over_ranks(v: float) -> float:
         if ws == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device=xdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -323,6 +358,10 @@ def run_ours(args, ws, rank, local):
     lds_peak_aes = peaks_live["lds_wavefronts_per_s"] / WAVEFRONTS_PER_AES
     alu_peak_aes = peaks_live["lop3_lane_ops_per_s"] / LOP3_PER_AES_BITSLICED
     secondary = measure_secondary(dev, args) if not args.no_secondary else None
+    if ws >= 2 and ws % 2 == 0 and not args.no_secondary:
+        secondary = dict(secondary or {})
+        secondary["nccl_masked_exchange"] = measure_exchange(dev, xdev, rank, ws, N, barrier,
+                                                             max_over_ranks)
     del out0, out1, rec
 
     # ---- e2e through the public API with host buffers ----------------------

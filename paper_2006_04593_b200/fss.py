@@ -67,7 +67,12 @@ class FssTape:
 
 
 def _index(idx, count: int, device):
-    """Normalise an index spec -> (slice | device LongTensor, numpy int64 indices)."""
+    """Normalise an index spec -> (slice | device LongTensor, host selector of
+    the ``consumed`` mask: a slice for contiguous ranges, else int64 indices)."""
+    if isinstance(idx, slice) and idx.step in (None, 1):
+        lo, hi, _ = idx.indices(count)
+        hi = max(hi, lo)
+        return slice(lo, hi), slice(lo, hi)
     if isinstance(idx, slice):
         arr = np.arange(count)[idx]
     elif isinstance(idx, torch.Tensor):
@@ -81,7 +86,7 @@ def _index(idx, count: int, device):
         return slice(0, 0), arr
     lo = int(arr[0])
     if arr.size == 1 or np.all(np.diff(arr) == 1):
-        return slice(lo, lo + arr.size), arr
+        return slice(lo, lo + arr.size), slice(lo, lo + arr.size)
     return torch.from_numpy(arr).to(device), arr
 
 

@@ -73,16 +73,25 @@ def relu_mask(session, x: AdditiveShare, cmp_keys: fss.CmpKeyBatch) -> AdditiveS
     return (-s).add_public(1)
 
 
+_OFF_DIAG = {}
+
+
+def _off_diagonal(m: int, device) -> torch.Tensor:
+    """Off-diagonal positions of an m x m block in row-major (j, i) order,
+    cached per device (building it per call would be a blocking H2D copy)."""
+    key = (m, str(device))
+    if key not in _OFF_DIAG:
+        idx = torch.arange(m * m, dtype=torch.int64, device=device)
+        _OFF_DIAG[key] = idx[idx // m != idx % m].contiguous()
+    return _OFF_DIAG[key]
+
+
 def _pairwise_diffs(data: torch.Tensor, m: int) -> torch.Tensor:
     """[..., j, i] = x_i - x_j with the diagonal removed, grouped by j
     (nn_ops.py:111-114): (..., m*(m-1))."""
     v = _dev.as_i64(data)
     diffs = (v[..., None, :] - v[..., :, None]).reshape(*v.shape[:-1], m * m)
-    # off-diagonal positions in row-major (j, i) order; index_select keeps the
-    # whole step on device (boolean-mask indexing would sync on nonzero())
-    off = torch.tensor([j * m + i for j in range(m) for i in range(m) if i != j],
-                       dtype=torch.int64, device=v.device)
-    return _dev.as_u64(diffs.index_select(-1, off))
+    return _dev.as_u64(diffs.index_select(-1, _off_diagonal(m, v.device)))
 
 
 def argmax(session, x: AdditiveShare, prep: ArgmaxPrep) -> AdditiveShare:

@@ -60,7 +60,13 @@ def test_pcg_jump_matches_numpy():
 def test_index_normalisation():
     from paper_2006_04593_b200.fss import _index
     sel, arr = _index(np.arange(3, 9), 10, None)
-    assert sel == slice(3, 9) and list(arr) == list(range(3, 9))
+    assert sel == slice(3, 9) and list(np.arange(10)[arr]) == list(range(3, 9))
+    sel, arr = _index(slice(4, None), 10, None)
+    assert sel == slice(4, 10) == arr
+    sel, arr = _index(slice(8, 3), 10, None)
+    assert np.arange(10)[arr].size == 0
+    sel, arr = _index(np.array([5, 1, 7]), 10, None)
+    assert list(arr) == [5, 1, 7]
     sel, arr = _index([-1], 10, None)
     assert sel == slice(9, 10)
     sel, arr = _index(range(2, 4), 10, None)
