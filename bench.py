@@ -197,7 +197,7 @@ def load_traffic():
     try:
         with open(path) as fh:
             d = json.load(fh)
-        return d.get("dram_bytes_per_party_eval")
+        return d.get("dram_bytes_per_unit", d.get("dram_bytes_per_party_eval"))
     except (OSError, ValueError):
         return None
 
@@ -435,7 +435,8 @@ def run_ours(args, ws, rank, local):
         "config": {"workload": f"DCF eval n=32 out_bits=32, 2^{args.log2n} keys per GPU, "
                                "both parties per step, keys resident in HBM",
                    "global_batch": ws * N, "seq_len": None, "parallelism": f"dp{ws} (element shards)",
-                   "l2": "inputs larger than L2 (18 GB of keys per GPU)"},
+                   "l2": "inputs larger than L2 (%.1f GB of keys per GPU, L2 126 MB)"
+                         % (N * (1064 + 2 * 24) / 1e9)},
         "roofline": {"bound": "smem-lookup", "achieved": aes_rate, "peak": lds_peak_aes,
                      "unit": "AES-blocks/s", "frac": aes_rate / lds_peak_aes,
                      "traffic": (traffic * N if traffic else None),
