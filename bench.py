@@ -41,8 +41,10 @@ N_BITS = 32
 BYTES_PER_EVAL = 16 + 32 * 16 + 32 + 32 * 8 + 33 * 8 + 8 + 8   # 1096 B
 AES_PER_EVAL = 64                                              # 32 levels x 2 blocks
 LDS_PER_AES = 160                                              # T-table lookups per block
-WAVEFRONTS_PER_AES = LDS_PER_AES / 32                          # one conflict-free LDS.32 wavefront
-                                                               # serves 32 lanes' lookups
+# Lookups the T-table DCF evaluation needs per party-eval: per level one full
+# block (160) + the sigma half-block (144 rounds 1-9 + 8 last-round) = 312.
+LOOKUPS_PER_EVAL = 32 * (160 + 152)                            # 9,984
+# one conflict-free LDS.32 wavefront serves 32 lanes' lookups
 LOP3_PER_AES_BITSLICED = 356.25                                # SURVEY.md §8d bitsliced floor
 
 
@@ -354,8 +356,9 @@ def run_ours(args, ws, rank, local):
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
     aes_rate = N * AES_PER_EVAL / avg_launch_s
+    lookup_rate = N * LOOKUPS_PER_EVAL / avg_launch_s
     peaks_live = _lib.probe_peaks()   # measured on this box, this run
-    lds_peak_aes = peaks_live["lds_wavefronts_per_s"] / WAVEFRONTS_PER_AES
+    lds_peak_lookups = peaks_live["lds_wavefronts_per_s"] * 32
     alu_peak_aes = peaks_live["lop3_lane_ops_per_s"] / LOP3_PER_AES_BITSLICED
     secondary = measure_secondary(dev, args) if not args.no_secondary else None
     if ws >= 2 and ws % 2 == 0 and not args.no_secondary:
@@ -437,16 +440,17 @@ def run_ours(args, ws, rank, local):
                    "global_batch": ws * N, "seq_len": None, "parallelism": f"dp{ws} (element shards)",
                    "l2": "inputs larger than L2 (%.1f GB of keys per GPU, L2 126 MB)"
                          % (N * (1064 + 2 * 24) / 1e9)},
-        "roofline": {"bound": "smem-lookup", "achieved": aes_rate, "peak": lds_peak_aes,
-                     "unit": "AES-blocks/s", "frac": aes_rate / lds_peak_aes,
+        "roofline": {"bound": "smem-lookup", "achieved": lookup_rate, "peak": lds_peak_lookups,
+                     "unit": "T-table lookups/s", "frac": lookup_rate / lds_peak_lookups,
                      "traffic": (traffic * N if traffic else None),
                      "kernel": "dcf_eval_kernel",
-                     "note": (f"{AES_PER_EVAL} AES blocks per party-eval x 2^{args.log2n} party-evals "
-                              "per launch / CUDA-event launch time; peak = measured conflict-free "
-                              f"LDS wavefront rate on this GPU ({peaks_live['lds_wavefronts_per_s']:.4g}/s, "
-                              f"fss_probe_peaks) / {WAVEFRONTS_PER_AES:g} wavefronts per AES block "
-                              "(160 T-table lookups); traffic = ncu DRAM bytes per launch "
-                              "(profiles/ncu_dcf_eval.json x N)")},
+                     "aes_blocks_per_s": aes_rate,
+                     "note": (f"{LOOKUPS_PER_EVAL} algorithmic lookups per party-eval (32 levels x "
+                              "[160 for the child block + 152 for the sigma half-block]) x "
+                              f"2^{args.log2n} party-evals per launch / CUDA-event launch time; "
+                              "peak = 32 x the measured conflict-free LDS wavefront rate on this GPU "
+                              f"({peaks_live['lds_wavefronts_per_s']:.4g}/s, fss_probe_peaks); "
+                              "traffic = ncu DRAM bytes per launch (profiles/ncu_dcf_eval.json x N)")},
         "alu_roofline": {"bound": "alu", "achieved": aes_rate, "peak": alu_peak_aes,
                          "unit": "AES-blocks/s", "frac": aes_rate / alu_peak_aes,
                          "note": (f"bitsliced-AES ALU roof of SURVEY.md 8d: measured LOP3 rate "

@@ -127,13 +127,14 @@ __device__ __forceinline__ uint32_t mixcol(uint32_t t0, uint32_t t1, uint32_t t2
     return t0 ^ t1 ^ t2 ^ t3 ^ rk<KEY, SEL>(w, m);
 }
 
-// One full AES-128 encryption of (c0..c3) (little-endian column words).
+// Rounds 0..9 of AES-128 on (c0..c3) (little-endian column words), in place.
 template <int KEY, bool SEL>
-__device__ __forceinline__ U4 aes128(const Tab& tb, U4 s, uint32_t m) {
-    uint32_t c0 = s.x ^ rk<KEY, SEL>(0, m);
-    uint32_t c1 = s.y ^ rk<KEY, SEL>(1, m);
-    uint32_t c2 = s.z ^ rk<KEY, SEL>(2, m);
-    uint32_t c3 = s.w ^ rk<KEY, SEL>(3, m);
+__device__ __forceinline__ void aes128_rounds(const Tab& tb, uint32_t& c0, uint32_t& c1, uint32_t& c2,
+                                              uint32_t& c3, uint32_t m) {
+    c0 ^= rk<KEY, SEL>(0, m);
+    c1 ^= rk<KEY, SEL>(1, m);
+    c2 ^= rk<KEY, SEL>(2, m);
+    c3 ^= rk<KEY, SEL>(3, m);
 #pragma unroll
     for (int r = 1; r < 10; r++) {
         const uint32_t n0 = mixcol<KEY, SEL>(T<0, 0>(tb, c0), T<1, 1>(tb, c1), T<2, 2>(tb, c2),
@@ -149,17 +150,46 @@ __device__ __forceinline__ U4 aes128(const Tab& tb, U4 s, uint32_t m) {
         c2 = n2;
         c3 = n3;
     }
-    // Last round: SubBytes+ShiftRows only. S(x) sits in byte r of Te_{(r+2)&3}[x].
+}
+
+// Last round (SubBytes + ShiftRows, no MixColumns) of output column c, whose
+// bytes come from columns (a, b, c, d) = (c, c+1, c+2, c+3): S(x) sits in
+// byte r of Te_{(r+2)&3}[x], so four lookups and three PRMTs build the word.
+__device__ __forceinline__ uint32_t last_col(const Tab& tb, uint32_t a, uint32_t b, uint32_t c,
+                                             uint32_t d) {
+    return __byte_perm(__byte_perm(T<2, 0>(tb, a), T<3, 1>(tb, b), 0x3250),
+                       __byte_perm(T<0, 2>(tb, c), T<1, 3>(tb, d), 0x7210), 0x7610);
+}
+
+// One full AES-128 encryption of (c0..c3) (little-endian column words).
+template <int KEY, bool SEL>
+__device__ __forceinline__ U4 aes128(const Tab& tb, U4 s, uint32_t m) {
+    uint32_t c0 = s.x, c1 = s.y, c2 = s.z, c3 = s.w;
+    aes128_rounds<KEY, SEL>(tb, c0, c1, c2, c3, m);
     U4 o;
-#define FSSB_LAST(a, b, c, d)                                                        \
-    __byte_perm(__byte_perm(T<2, 0>(tb, a), T<3, 1>(tb, b), 0x3250),                 \
-                __byte_perm(T<0, 2>(tb, c), T<1, 3>(tb, d), 0x7210), 0x7610)
-    o.x = FSSB_LAST(c0, c1, c2, c3) ^ rk<KEY, SEL>(40, m);
-    o.y = FSSB_LAST(c1, c2, c3, c0) ^ rk<KEY, SEL>(41, m);
-    o.z = FSSB_LAST(c2, c3, c0, c1) ^ rk<KEY, SEL>(42, m);
-    o.w = FSSB_LAST(c3, c0, c1, c2) ^ rk<KEY, SEL>(43, m);
-#undef FSSB_LAST
+    o.x = last_col(tb, c0, c1, c2, c3) ^ rk<KEY, SEL>(40, m);
+    o.y = last_col(tb, c1, c2, c3, c0) ^ rk<KEY, SEL>(41, m);
+    o.z = last_col(tb, c2, c3, c0, c1) ^ rk<KEY, SEL>(42, m);
+    o.w = last_col(tb, c3, c0, c1, c2) ^ rk<KEY, SEL>(43, m);
     return o;
+}
+
+// MMO block AES_KEY(s) ^ s, but only its 8-byte half `h` (0: bytes 0..7,
+// 1: bytes 8..15; hm = 0 - h). The last round then needs 8 of the 16 lookups:
+// DCF evaluation reads only the sigma/tau lane x_i of the third block
+// (slice_cmp, prg.py:99-119), so this is exact. Returns (lo, hi) words.
+template <int KEY>
+__device__ __forceinline__ void mmo_half(const Tab& tb, U4 s, uint32_t hm, uint32_t& lo,
+                                         uint32_t& hi) {
+    uint32_t c0 = s.x, c1 = s.y, c2 = s.z, c3 = s.w;
+    aes128_rounds<KEY, false>(tb, c0, c1, c2, c3, 0);
+    // rotate the columns by 2*h: output columns (2h, 2h+1) = last_col of (a0..a3), (a1..a0)
+    const uint32_t a0 = hm ? c2 : c0, a1 = hm ? c3 : c1, a2 = hm ? c0 : c2, a3 = hm ? c1 : c3;
+    const uint32_t k_lo = kRK[KEY][40] ^ (hm & (kRK[KEY][40] ^ kRK[KEY][42]));
+    const uint32_t k_hi = kRK[KEY][41] ^ (hm & (kRK[KEY][41] ^ kRK[KEY][43]));
+    const uint32_t s_lo = hm ? s.z : s.x, s_hi = hm ? s.w : s.y;
+    lo = lop3_xor3(last_col(tb, a0, a1, a2, a3), k_lo, s_lo);
+    hi = lop3_xor3(last_col(tb, a1, a2, a3, a0), k_hi, s_hi);
 }
 
 // Matyas-Meyer-Oseas block: AES_k(s) XOR s  (reference prg.expand, prg.py:43-60).

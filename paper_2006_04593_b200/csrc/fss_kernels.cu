@@ -210,13 +210,14 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
 #endif
             const uint32_t xb = (uint32_t)(xe >> (n - 1 - i)) & 1u;
             const U4 a = fssb::mmo<0, true>(tb, s, 0u - xb);
-            const U4 g = fssb::mmo<2, false>(tb, s, 0);
             const uint32_t tm = 0u - t;
-            // sigma/tau lane x_i of the third block (slice_cmp, prg.py:99-119)
-            const uint32_t lane_hi = xb ? g.w : g.y;
+            // sigma/tau lane x_i of the third block (slice_cmp, prg.py:99-119):
+            // only that 8-byte half of AES_k3(s) ^ s is computed
+            uint32_t lane_lo, lane_hi;
+            fssb::mmo_half<2>(tb, s, 0u - xb, lane_lo, lane_hi);
             W lane;
-            if (W32) lane = (W)(xb ? g.z : g.x);
-            else lane = (W)(xb ? hi64(g) : lo64(g));
+            if (W32) lane = (W)lane_lo;
+            else lane = (W)(((uint64_t)lane_hi << 32) | lane_lo);
             const uint32_t tau = ((lane_hi >> 31) ^ (t & (f >> (2 + xb)))) & 1u;
             const W sigma = lane ^ (sig & (W)(0 - (W)t));
             const W oi = (leaf & (W)(0 - (W)tau)) + sigma;

@@ -19,7 +19,6 @@ VDIR = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = {
     "default": [],
-    "w64": ["FSSB_W32=0"],
 }
 # round-1 sweep b (profiles/r01_aes_variants_b.json): 512/640/768/1024 threads
 # x prefetch; more resident warps win (1024: DCF 92.9 %, DPF 85.5 % of the
@@ -73,7 +72,9 @@ def run(log2n: int):
             assert rc == 0
 
         row = {}
-        for kname, fn, ref, aes in (("dcf_eval", dcf, ref0, 64), ("dpf_eval", dpf, ref_e, 32)):
+        # lookups per party-eval: DCF 32 x (160 + 152: sigma half-block), DPF 32 x 160
+        for kname, fn, ref, aes, lk in (("dcf_eval", dcf, ref0, 64, 9984),
+                                        ("dpf_eval", dpf, ref_e, 32, 5120)):
             fn()
             torch.cuda.synchronize()
             assert torch.equal(res.view(torch.int64), ref.view(torch.int64)), (name, kname)
@@ -87,7 +88,7 @@ def run(log2n: int):
                 ts.append(a.elapsed_time(b) / 1e3)
             t = sorted(ts)[len(ts) // 2]
             row[kname] = {"ms": t * 1e3, "party_evals_per_s": N / t, "aes_per_s": N * aes / t,
-                          "frac_lds_roof": N * aes / t / (peaks["lds_wavefronts_per_s"] / 5)}
+                          "frac_lds_roof": N * lk / t / (peaks["lds_wavefronts_per_s"] * 32)}
         out[name] = row
         print(name, json.dumps(row), flush=True)
     # T-table vs bitsliced AES on the PRG expand (2^24 seeds, 3 blocks each)
