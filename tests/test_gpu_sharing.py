@@ -134,3 +134,20 @@ def test_batched_maxpool_is_the_plaintext_max(route):
     assert got.shape == (P, m // 2, m // 2)
     assert np.mean(np.abs(got - want) < 1e-9) > 0.99
     assert l0.total_rounds() == (3 if route == "argmax" else 4)
+
+
+def test_triple_container_bytes_match_reference():
+    # kind-2 ARNK container of an elementwise triple (beaver.py:319-330), bytes
+    # produced by the reference for the same rng seed (tests/golden/triple_arnk.npz)
+    import os
+
+    from conftest import GOLDEN
+    from paper_2006_04593_b200 import fss
+    with np.load(os.path.join(GOLDEN, "triple_arnk.npz")) as g:
+        want, seed = g["arnk"].tobytes(), int(g["seed"])
+    rng = np.random.default_rng(seed)
+    t0, t1 = beaver.gen_triple(beaver.OP_MUL, beaver.ElemwiseGeometry((3, 4)), 32, rng)
+    blob = fss.serialize_keys(beaver.pack_triples(t0, t1))
+    assert blob == want
+    u0, u1 = beaver.unpack_triples(fss.deserialize_keys(blob))
+    assert u0.a == t0.a and u1.b == t1.b and u1.c == t1.c
