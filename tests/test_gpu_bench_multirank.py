@@ -1,0 +1,40 @@
+"""bench.py's N>1 code path (torchrun, one process per rank, max-over-ranks
+timing, the NCCL masked-exchange secondary) exercised on a single-GPU box:
+FSS_BENCH_SAME_GPU=1 puts both ranks on cuda:0 over gloo. Only the contract
+is checked -- numbers from two ranks sharing one GPU are meaningless."""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU containers
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+def test_two_rank_bench_contract():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, FSS_BENCH_SAME_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        str(port), os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3",
+                        "--warmup", "3", "--log2n", "18"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1                        # rank 0 prints one line
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["config"]["global_batch"] == 2 << 18
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] == 6
+    ex = d["secondary"]["nccl_masked_exchange"]
+    assert ex["bytes_each_way_per_rank"] == 4 << 18 and ex["pairs"] == 1

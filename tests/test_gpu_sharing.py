@@ -151,3 +151,27 @@ def test_triple_container_bytes_match_reference():
     assert blob == want
     u0, u1 = beaver.unpack_triples(fss.deserialize_keys(blob))
     assert u0.a == t0.a and u1.b == t1.b and u1.c == t1.c
+
+
+@pytest.mark.parametrize("n", [6, 8, 12])
+def test_protocols_at_narrow_rings(n):
+    # masked messages at 1- and 2-byte wire widths, opened inside the eval kernels
+    from paper_2006_04593_b200 import fss
+    rng = np.random.default_rng(n)
+    vals = rng.integers(-2, 3, 4000)
+    ys = sharing.share(RingTensor.from_ints(vals, n), rng)
+    d = dealer.make_dealer(n, seed=n + 1)
+
+    def prog(s):
+        view = d.for_party(s.party)
+        e = fss.eq_protocol(s, ys[s.party], view.eq_keys(4000))
+        c = fss.sign_protocol(s, ys[s.party], view.cmp_keys(4000))
+        return e, c
+    ((e0, c0), l0), ((e1, c1), _) = runtime.run_local_pair(prog)
+    assert l0.bytes_sent == {"equality": 4000 * (1 if n <= 8 else 2),
+                             "comparison": 4000 * (1 if n <= 8 else 2)}
+    eq = sharing.reconstruct(e0, e1).numpy()
+    assert np.array_equal(eq, (vals == 0).astype(np.uint64))
+    cmp = sharing.reconstruct(c0, c1).numpy()
+    # sign test fails with probability |y| / 2^n per element (fss.py:444-473)
+    assert np.mean(cmp != (vals <= 0).astype(np.uint64)) < 8 * 2.0 / 2 ** n + 0.01
