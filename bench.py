@@ -157,7 +157,7 @@ def run_reference(args, ws, rank):
         "impl": "reference", "metric": "FSS comparisons/sec (DCF eval, n=32)", "value": v,
         "unit": "comparisons/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u64", "data": "synthetic",
+        "dtype": "u32", "data": "synthetic",
         "config": {"workload": f"DCF eval n=32, both parties, bounded CPU sample of 2^{args.cpu_log2n} "
                                f"keys (the GPU arm runs 2^{args.log2n} per GPU)",
                    "global_batch": N, "parallelism": f"{cores} host threads"},
@@ -434,10 +434,12 @@ def run_ours(args, ws, rank, local):
         "metric": "FSS comparisons/sec (DCF eval, n=32)",
         "value": value, "unit": "comparisons/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "dtype_note": "AES on 32-bit words / u8 key bytes, ring sums mod 2^32 (u64 storage, "
+                      "reference layout)", "data": "synthetic",
         "config": {"workload": f"DCF eval n=32 out_bits=32, 2^{args.log2n} keys per GPU, "
                                "both parties per step, keys resident in HBM",
-                   "global_batch": ws * N, "seq_len": None, "parallelism": f"dp{ws} (element shards)",
+                   "global_batch": ws * N, "parallelism": f"dp{ws} (element shards)",
                    "l2": "inputs larger than L2 (%.1f GB of keys per GPU, L2 126 MB)"
                          % (N * (1064 + 2 * 24) / 1e9)},
         "roofline": {"bound": "smem-lookup", "achieved": lookup_rate, "peak": lds_peak_lookups,
