@@ -51,6 +51,13 @@ int fss_abi_version(void);
 int fss_aes_mmo_expand(const uint8_t* seeds, uint64_t count, int out_blocks, uint8_t* out,
                        void* stream);
 
+/* prg.mask_stream (prg.py:128-147): count ring elements mod 2^n_bits of the
+ * aggregation-mask stream for a 16-byte seed (seed_lo = LE bytes 0..7,
+ * seed_hi = bytes 8..15) and a round counter; block i = seed ^ (round || i),
+ * top bit cleared, 2-block MMO expansion -> 4 u64 lanes. */
+int fss_mask_stream(uint64_t seed_lo, uint64_t seed_hi, uint64_t round_idx, uint64_t count,
+                    int n_bits, uint64_t* out, void* stream);
+
 /* Same result as fss_aes_mmo_expand through the bitsliced AES
  * (csrc/aes_bitsliced.cuh) instead of T-tables: the measured alternative
  * SURVEY.md 8d proposed. count must be a multiple of 32. */

@@ -38,6 +38,7 @@ SIGNATURES = {
     "fss_last_error": [],
     "fss_aes_mmo_expand": [_vp, _u64, _int, _vp, _vp],
     "fss_aes_mmo_expand_bitsliced": [_vp, _u64, _int, _vp, _vp],
+    "fss_mask_stream": [_u64, _u64, _u64, _u64, _int, _vp, _vp],
     "fss_pcg64_tape": [ctypes.POINTER(PcgState), _int, _u64, _int, _vp, _vp, _vp, _vp,
                        ctypes.POINTER(PcgState), _vp],
     "fss_pcg64_ring_random": [ctypes.POINTER(PcgState), _int, _u64, _vp, ctypes.POINTER(PcgState), _vp],

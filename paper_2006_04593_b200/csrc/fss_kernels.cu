@@ -103,6 +103,31 @@ __device__ __forceinline__ uint64_t load_x(const uint64_t* __restrict__ x, const
     return fssb::wire_get(wb, m_own, e) + fssb::wire_get(wb, m_peer, e);
 }
 
+// ------------------------------------------------------------- mask stream
+// prg.mask_stream (prg.py:128-147): counter-mode use of G. Block i is the seed
+// XOR (round_idx LE in bytes 0..7, i LE in bytes 8..15) with the top bit of
+// byte 15 re-cleared; G(block) = AES_k1 ^ . || AES_k2 ^ . gives 4 u64 lanes =
+// ring elements 4i .. 4i+3.
+__global__ void __launch_bounds__(kKeygenThreads, 1)
+mask_stream_kernel(U4 seed, uint64_t round_idx, uint64_t blocks, uint64_t count, uint64_t mask,
+                   uint64_t* __restrict__ out) {
+    extern __shared__ uint32_t tab[];
+    fssb::fill_tables(tab);
+    __syncthreads();
+    const fssb::Tab tb = fssb::make_tab(tab);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < blocks;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        U4 b = U4{seed.x ^ (uint32_t)round_idx, seed.y ^ (uint32_t)(round_idx >> 32),
+                  seed.z ^ (uint32_t)i, seed.w ^ (uint32_t)(i >> 32)};
+        b.w &= 0x7FFFFFFFu;
+        const U4 l = fssb::mmo<0, false>(tb, b, 0), r = fssb::mmo<1, false>(tb, b, 0);
+        const uint64_t lanes[4] = {lo64(l), hi64(l), lo64(r), hi64(r)};
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+            if (4 * i + j < count) out[4 * i + j] = lanes[j] & mask;
+    }
+}
+
 // ---------------------------------------------------------------- DPF eval
 // fss.eval_eq (fss.py:357-377): t0 = party, per level expand, correct with
 // scw/tcw when t, descend to child x_i (MSB first); out = t*cw_final + s2r(s).
@@ -528,6 +553,8 @@ int prep_launch(K kernel, int* grid) {
     return kOk;
 }
 
+uint64_t ring_mask_host(int w) { return w >= 64 ? ~0ULL : ((1ULL << w) - 1); }
+
 int grid_for(uint64_t count, int sms, int threads) {
     const uint64_t need = (count + threads - 1) / threads;
     return (int)(need < (uint64_t)sms ? (need ? need : 1) : sms);
@@ -710,6 +737,21 @@ int fss_pcg64_tape(const fss_pcg64_state* st, int n, uint64_t count, int draw_al
     const int bs = 256;
     const uint64_t grid = threads ? (threads + bs - 1) / bs : 1;
     pcg64_tape_kernel<<<(unsigned)grid, bs, 0, (cudaStream_t)stream>>>(P, alpha, alpha0, s0, s1);
+    return check_launch();
+}
+
+int fss_mask_stream(uint64_t seed_lo, uint64_t seed_hi, uint64_t round_idx, uint64_t count,
+                    int n_bits, uint64_t* out, void* stream) {
+    if (n_bits < 1 || n_bits > 64) return set_err(kEinval, "ring width out of range%s");
+    if (count == 0) return kOk;
+    int sms;
+    if (int rc = prep_launch(mask_stream_kernel, &sms)) return rc;
+    const uint64_t blocks = (count + 3) / 4;
+    const U4 seed = U4{(uint32_t)seed_lo, (uint32_t)(seed_lo >> 32), (uint32_t)seed_hi,
+                       (uint32_t)(seed_hi >> 32)};
+    mask_stream_kernel<<<grid_for(blocks, sms, kKeygenThreads), kKeygenThreads, fssb::kTableBytes,
+                         (cudaStream_t)stream>>>(seed, round_idx, blocks, count, ring_mask_host(n_bits),
+                                                 out);
     return check_launch();
 }
 

@@ -145,3 +145,22 @@ def seed_to_ring(seeds, n: int):
         v = v & mask
     v = v.view(torch.uint64)
     return _dev.to_numpy(v) if host else v
+
+
+def mask_stream(seed: bytes, round_idx: int, count: int, n_bits: int, device=None):
+    """Deterministic ring-element stream for aggregation masks (prg.py:128-147):
+    block i = seed ^ (round_idx LE bytes 0..7 || i LE bytes 8..15), top bit
+    re-cleared, expanded to 2 MMO blocks = 4 u64 lanes. One fused kernel
+    (fss_mask_stream); returns numpy like the reference unless ``device``
+    is given, in which case the device tensor is returned."""
+    if len(seed) != BLOCK_BYTES:
+        raise ValueError("seed must be 16 bytes")
+    ring_mask(n_bits)
+    dev = _dev.default_device(device)
+    lo = int.from_bytes(bytes(seed[:8]), "little")
+    hi = int.from_bytes(bytes(seed[8:]), "little")
+    out = torch.empty(int(count), dtype=torch.uint64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.call("fss_mask_stream", lo, hi, int(round_idx) & _dev.FULL64, int(count), n_bits,
+                  _dev.ptr(out), _dev.stream_handle(dev))
+    return out if device is not None else _dev.to_numpy(out)

@@ -329,3 +329,16 @@ def test_ring_random_on_device_matches_numpy(pre, shape, n_bits):
     assert t.data.is_cuda and tuple(t.shape) == tuple(shape)
     assert np.array_equal(t.numpy(), raw & mask)
     assert a.bit_generator.state == b.bit_generator.state
+
+
+def test_mask_stream_matches_reference():
+    # prg.mask_stream (prg.py:128-147) vectors produced by the reference
+    with np.load(os.path.join(GOLDEN, "mask_stream.npz")) as g:
+        for i in range(int(g["cases"])):
+            rnd, count, n = (int(v) for v in g[f"meta{i}"])
+            got = prg.mask_stream(g[f"seed{i}"].tobytes(), rnd, count, n)
+            assert isinstance(got, np.ndarray) and np.array_equal(got, g[f"out{i}"]), i
+    a = prg.mask_stream(bytes(range(16)), 0, 100, 32)
+    assert not np.array_equal(a, prg.mask_stream(bytes(range(16)), 1, 100, 32))
+    with pytest.raises(ValueError):
+        prg.mask_stream(bytes(15), 0, 4, 32)
