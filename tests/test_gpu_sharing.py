@@ -175,3 +175,16 @@ def test_protocols_at_narrow_rings(n):
     cmp = sharing.reconstruct(c0, c1).numpy()
     # sign test fails with probability |y| / 2^n per element (fss.py:444-473)
     assert np.mean(cmp != (vals <= 0).astype(np.uint64)) < 8 * 2.0 / 2 ** n + 0.01
+
+
+@pytest.mark.parametrize("n", [4, 13, 32, 63, 64])
+def test_bit_decompose_recompose(n):
+    from paper_2006_04593_b200.ring import bit_decompose, recompose
+    rng = np.random.default_rng(n)
+    a = rng.integers(0, np.iinfo(np.uint64).max, (5, 7), dtype=np.uint64, endpoint=True) & _u(n)
+    A = RingTensor(a, n)
+    bits = bit_decompose(A).cpu().numpy()
+    want = np.stack([((a >> np.uint64(n - 1 - i)) & np.uint64(1)).astype(np.uint8)
+                     for i in range(n)])
+    assert np.array_equal(bits, want)
+    assert recompose(bits, n) == A
