@@ -73,6 +73,12 @@ int fss_pcg64_tape(const fss_pcg64_state* st, int n, uint64_t count, int draw_al
                    uint64_t* alpha, uint64_t* alpha0, uint8_t* s0, uint8_t* s1,
                    fss_pcg64_state* st_out, void* stream);
 
+/* The two random_seeds draws of _sample_tape alone (prg.py:36-40; s0 then s1)
+ * -- the tail of the n = 64 tape, whose alpha / alpha0 are drawn by
+ * fss_pcg64_ring_random (fss._uniform_ring's n == 64 branch, fss.py:48-50). */
+int fss_pcg64_seeds(const fss_pcg64_state* st, uint64_t count, uint8_t* s0, uint8_t* s1,
+                    fss_pcg64_state* st_out, void* stream);
+
 /* RingTensor.random (ring.py:61-65) through numpy's PCG64 Generator:
  * out[i] = ((integers(0, 2^63)[i] << 1) | integers(0, 2)[i]) mod 2^n_bits,
  * bit-identical to the reference's draws (both the 64-bit and the buffered

@@ -417,6 +417,7 @@ struct TapePlan {
     int n;
     uint64_t count;
     int draw_alpha;    // alpha drawn (1) or given (0)
+    int draw_alpha0;   // alpha0 drawn (1) or not (0: seeds-only tape)
     int has_uint32;    // numpy's buffered half-word present at start
     uint32_t uinteger;
     uint64_t raw64;    // number of 64-bit draws before the 32-bit stream (n > 32)
@@ -436,8 +437,10 @@ __device__ __forceinline__ void emit_word(const TapePlan& P, uint64_t w, uint32_
             if (k < N) { alpha[k] = (uint64_t)(v >> sh); return; }
             k -= N;
         }
-        if (k < N) { alpha0[k] = (uint64_t)(v >> sh); return; }
-        k -= N;
+        if (P.draw_alpha0) {
+            if (k < N) { alpha0[k] = (uint64_t)(v >> sh); return; }
+            k -= N;
+        }
     }
     // seeds: 4 words per seed, byte 15 top bit cleared (prg.random_seeds, prg.py:36-40)
     uint8_t* dst = k < 4 * N ? s0 : s1;
@@ -701,22 +704,26 @@ int fss_dcf_keygen(int n, int out_bits, uint64_t count, const uint64_t* alpha,
     return check_launch();
 }
 
-int fss_pcg64_tape(const fss_pcg64_state* st, int n, uint64_t count, int draw_alpha,
-                   uint64_t* alpha, uint64_t* alpha0, uint8_t* s0, uint8_t* s1,
-                   fss_pcg64_state* st_out, void* stream) {
-    if (n < 1 || n > 63) return set_err(kEinval, "device tape supports n <= 63%s");
+}  // extern "C"
+
+namespace {
+
+int launch_tape(const fss_pcg64_state* st, int n, uint64_t count, int draw_alpha, int draw_alpha0,
+                uint64_t* alpha, uint64_t* alpha0, uint8_t* s0, uint8_t* s1, fss_pcg64_state* st_out,
+                void* stream) {
     TapePlan P;
     P.state_lo = st->state_lo; P.state_hi = st->state_hi;
     P.inc_lo = st->inc_lo; P.inc_hi = st->inc_hi;
     P.n = n; P.count = count; P.draw_alpha = draw_alpha ? 1 : 0;
+    P.draw_alpha0 = draw_alpha0 ? 1 : 0;
     P.has_uint32 = st->has_uint32 ? 1 : 0;
     P.uinteger = st->uinteger;
-    const uint64_t na = P.draw_alpha ? count : 0;
+    const uint64_t na = (P.draw_alpha ? count : 0) + (P.draw_alpha0 ? count : 0);
     if (n <= 32) {
         P.raw64 = 0;
-        P.words = na + count + 8 * count;
+        P.words = na + 8 * count;
     } else {
-        P.raw64 = na + count;
+        P.raw64 = na;
         P.words = 8 * count;
     }
     const uint64_t h = (uint64_t)P.has_uint32;
@@ -740,6 +747,22 @@ int fss_pcg64_tape(const fss_pcg64_state* st, int n, uint64_t count, int draw_al
     return check_launch();
 }
 
+}  // namespace
+
+extern "C" {
+
+int fss_pcg64_tape(const fss_pcg64_state* st, int n, uint64_t count, int draw_alpha,
+                   uint64_t* alpha, uint64_t* alpha0, uint8_t* s0, uint8_t* s1,
+                   fss_pcg64_state* st_out, void* stream) {
+    if (n < 1 || n > 63) return set_err(kEinval, "device tape supports n <= 63%s");
+    return launch_tape(st, n, count, draw_alpha, 1, alpha, alpha0, s0, s1, st_out, stream);
+}
+
+int fss_pcg64_seeds(const fss_pcg64_state* st, uint64_t count, uint8_t* s0, uint8_t* s1,
+                    fss_pcg64_state* st_out, void* stream) {
+    return launch_tape(st, 32, count, 0, 0, nullptr, nullptr, s0, s1, st_out, stream);
+}
+
 int fss_mask_stream(uint64_t seed_lo, uint64_t seed_hi, uint64_t round_idx, uint64_t count,
                     int n_bits, uint64_t* out, void* stream) {
     if (n_bits < 1 || n_bits > 64) return set_err(kEinval, "ring width out of range%s");
@@ -761,7 +784,7 @@ int fss_pcg64_ring_random(const fss_pcg64_state* st, int n_bits, uint64_t count,
     TapePlan P;
     P.state_lo = st->state_lo; P.state_hi = st->state_hi;
     P.inc_lo = st->inc_lo; P.inc_hi = st->inc_hi;
-    P.n = n_bits; P.count = count; P.draw_alpha = 0;
+    P.n = n_bits; P.count = count; P.draw_alpha = 0; P.draw_alpha0 = 0;
     P.has_uint32 = st->has_uint32 ? 1 : 0;
     P.uinteger = st->uinteger;
     P.raw64 = count;

@@ -255,9 +255,24 @@ def _sample_tape(n: int, rng, count: int, alpha, device):
             raise ValueError("alpha must have shape (count,)")
         from . import ring_ops
         alpha_t = ring_ops.mask(alpha_t, n)
+    if n == 64 and _pcg.is_pcg64(rng):
+        # fss._uniform_ring's n == 64 branch (fss.py:48-50) is RingTensor.random's
+        # two-call draw: the ring kernel, then the seeds-only tape
+        from .ring import RingTensor
+        a = alpha_t if alpha is not None else RingTensor.random((count,), 64, rng, device).data
+        a0 = RingTensor.random((count,), 64, rng, device).data
+        s0 = torch.empty((count, 16), dtype=torch.uint8, device=device)
+        s1 = torch.empty((count, 16), dtype=torch.uint8, device=device)
+        cst, st = _pcg.snapshot(rng)
+        out_st = PcgState()
+        with torch.cuda.device(device):
+            _lib.call("fss_pcg64_seeds", cst, count, _dev.ptr(s0), _dev.ptr(s1), out_st,
+                      _dev.stream_handle(device))
+        _pcg.commit(rng, st, out_st, count > 0)
+        return a, a0, s0, s1
     if not _device_tape_ok(n, rng):
-        # n = 64 (two-call uniform draw, fss.py:48-50) or a non-PCG64 generator:
-        # the randomness source itself is host numpy, exactly the reference's calls.
+        # a non-PCG64 bit generator (MT19937, Philox, ...): the randomness source
+        # is the caller's own host generator, drawn with the reference's calls.
         return _sample_tape_host(n, rng, count, alpha_t if alpha is not None else None, device)
     cst, st = _pcg.snapshot(rng)
     out_st = PcgState()

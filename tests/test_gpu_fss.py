@@ -342,3 +342,18 @@ def test_mask_stream_matches_reference():
     assert not np.array_equal(a, prg.mask_stream(bytes(range(16)), 1, 100, 32))
     with pytest.raises(ValueError):
         prg.mask_stream(bytes(15), 0, 4, 32)
+
+
+@pytest.mark.parametrize("pre", [0, 1])
+def test_n64_tape_on_device_matches_numpy(oracle, pre):
+    # n = 64 keys: alpha/alpha0 via the ring kernel (two-call uniform draw,
+    # fss.py:48-50) and the seeds-only PCG64 tape; the caller's rng state after
+    # keygen must equal numpy's
+    rng, ref = np.random.default_rng(64), np.random.default_rng(64)
+    rng.integers(0, 2, size=pre, dtype=np.uint64)
+    ref.integers(0, 2, size=pre, dtype=np.uint64)
+    alpha, k0, k1 = fss.keygen_eq(64, rng, 257)
+    a, a0, s0, s1 = oracle.sample_tape(64, ref, 257)
+    assert np.array_equal(_np(alpha), a) and np.array_equal(_np(k0.alpha_share), a0)
+    assert np.array_equal(_np(k0.seed0), s0) and np.array_equal(_np(k1.seed0), s1)
+    assert rng.bit_generator.state == ref.bit_generator.state
