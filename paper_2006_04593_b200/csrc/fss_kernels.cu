@@ -644,6 +644,40 @@ int launch_dcf_eval(int party, int n, int out_bits, uint64_t count, uint64_t ld,
     return check_launch();
 }
 
+// Host-buffer evaluation as one native call: the element range is streamed in
+// chunks over two CUDA streams -- H2D of x (pinned host), the eval kernel, D2H
+// of the shares (pinned host) -- so the copies of one chunk overlap the kernel
+// of the other. Chunks alternate streams and each stream reuses its own slot of
+// the caller's device scratch (2 * chunk words each for x and out), which stream
+// order makes safe. Returns after enqueueing; the caller synchronises.
+struct HostPipe {
+    const uint64_t* x_host;
+    uint64_t* out_host;
+    uint64_t* x_dev;
+    uint64_t* out_dev;
+    uint64_t chunk;
+    cudaStream_t st[2];
+};
+
+template <typename Launch>
+int run_host_pipe(const HostPipe& hp, uint64_t count, Launch launch) {
+    if (!hp.x_host || !hp.out_host || !hp.x_dev || !hp.out_dev || hp.chunk == 0)
+        return set_err(kEinval, "pipelined eval needs host/device buffers and a chunk size%s");
+    for (uint64_t i = 0, lo = 0; lo < count; i++, lo += hp.chunk) {
+        const uint64_t m = count - lo < hp.chunk ? count - lo : hp.chunk;
+        const int slot = (int)(i & 1);
+        cudaStream_t s = hp.st[slot];
+        uint64_t* xd = hp.x_dev + slot * hp.chunk;
+        uint64_t* od = hp.out_dev + slot * hp.chunk;
+        cudaError_t err = cudaMemcpyAsync(xd, hp.x_host + lo, m * 8, cudaMemcpyHostToDevice, s);
+        if (err != cudaSuccess) return set_err(kEcuda, "H2D: %s", cudaGetErrorString(err));
+        if (int rc = launch(lo, m, xd, od, s)) return rc;
+        err = cudaMemcpyAsync(hp.out_host + lo, od, m * 8, cudaMemcpyDeviceToHost, s);
+        if (err != cudaSuccess) return set_err(kEcuda, "D2H: %s", cudaGetErrorString(err));
+    }
+    return kOk;
+}
+
 }  // namespace
 
 extern "C" {
@@ -668,6 +702,33 @@ int fss_dcf_eval(int party, int n, int out_bits, uint64_t count, uint64_t ld, co
                  void* stream) {
     return launch_dcf_eval(party, n, out_bits, count, ld, seed0, scw, tcw, sigma_cw, leaf_cw, x, nullptr,
                            nullptr, out, levels, stream);
+}
+
+int fss_dcf_eval_host(int party, int n, int out_bits, uint64_t count, uint64_t ld,
+                      const uint8_t* seed0, const uint8_t* scw, const uint8_t* tcw,
+                      const uint64_t* sigma_cw, const uint64_t* leaf_cw, const uint64_t* x_host,
+                      uint64_t* out_host, uint64_t* x_dev, uint64_t* out_dev, uint64_t chunk,
+                      void* stream_a, void* stream_b) {
+    const HostPipe hp{x_host, out_host, x_dev, out_dev, chunk,
+                      {(cudaStream_t)stream_a, (cudaStream_t)stream_b}};
+    return run_host_pipe(hp, count, [&](uint64_t lo, uint64_t m, const uint64_t* xd, uint64_t* od,
+                                        cudaStream_t s) {
+        return launch_dcf_eval(party, n, out_bits, m, ld, seed0 + 16 * lo, scw + 16 * lo, tcw + lo,
+                               sigma_cw + lo, leaf_cw + lo, xd, nullptr, nullptr, od, nullptr, s);
+    });
+}
+
+int fss_dpf_eval_host(int party, int n, uint64_t count, uint64_t ld, const uint8_t* seed0,
+                      const uint8_t* scw, const uint8_t* tcw, const uint64_t* cw_final,
+                      const uint64_t* x_host, uint64_t* out_host, uint64_t* x_dev, uint64_t* out_dev,
+                      uint64_t chunk, void* stream_a, void* stream_b) {
+    const HostPipe hp{x_host, out_host, x_dev, out_dev, chunk,
+                      {(cudaStream_t)stream_a, (cudaStream_t)stream_b}};
+    return run_host_pipe(hp, count, [&](uint64_t lo, uint64_t m, const uint64_t* xd, uint64_t* od,
+                                        cudaStream_t s) {
+        return launch_dpf_eval(party, n, m, ld, seed0 + 16 * lo, scw + 16 * lo, tcw + lo,
+                               cw_final + lo, xd, nullptr, nullptr, od, s);
+    });
 }
 
 int fss_dcf_eval_masked(int party, int n, int out_bits, uint64_t count, uint64_t ld,

@@ -450,31 +450,32 @@ PIPELINE_MIN = 1 << 21
 PIPELINE_CHUNK = 1 << 20
 
 
-def _run_eval(launch, xt, host, count: int, dev):
-    """Run ``launch(lo, hi, x_dev, out_dev, stream)`` over [0, count).
+def _run_eval(launch, xt, host, count: int, dev, host_launch=None):
+    """Run the evaluation over [0, count).
 
-    Device (or numpy) input: one launch on the current stream. Pinned host
-    torch input: a 2-stream chunked pipeline that returns a pinned host tensor."""
-    if host != "torch_pinned" or count < PIPELINE_MIN:
+    Device (or numpy) input: ``launch(lo, hi, x_dev, out_dev, stream)`` once on
+    the current stream. Pinned host torch input: ``host_launch(x_host, out_host,
+    x_scratch, out_scratch, chunk, stream_a, stream_b)`` -- one native call
+    (fss_*_eval_host) that streams chunks over two CUDA streams so the H2D copy,
+    the kernel and the D2H copy of consecutive chunks overlap; returns a pinned
+    host tensor."""
+    if host != "torch_pinned" or count < PIPELINE_MIN or host_launch is None:
         if host == "torch_pinned":
             xt = xt.to(dev, non_blocking=True)
         out = torch.empty(count, dtype=torch.uint64, device=dev)
         launch(0, count, xt, out, _dev.stream_handle(dev))
         return _result(out, "torch" if host == "torch_pinned" else host)
+    chunk = PIPELINE_CHUNK
     out_host = torch.empty(count, dtype=torch.uint64, pin_memory=True)
     cur = torch.cuda.current_stream(dev)
+    # scratch on the current stream; the side streams wait for it and the
+    # current stream waits for them, so the allocator cannot recycle it early
+    scratch = torch.empty((2, 2 * chunk), dtype=torch.uint64, device=dev)
     streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
     for st in streams:
         st.wait_stream(cur)
-    xs64, os64 = xt.view(torch.int64), out_host.view(torch.int64)
-    for i, lo in enumerate(range(0, count, PIPELINE_CHUNK)):
-        hi = min(count, lo + PIPELINE_CHUNK)
-        st = streams[i & 1]
-        with torch.cuda.stream(st):
-            xd = xs64[lo:hi].to(dev, non_blocking=True)
-            od = torch.empty(hi - lo, dtype=torch.int64, device=dev)
-            launch(lo, hi, xd, od, st.cuda_stream)
-            os64[lo:hi].copy_(od, non_blocking=True)
+    host_launch(xt, out_host, scratch[0], scratch[1], chunk, streams[0].cuda_stream,
+                streams[1].cuda_stream)
     for st in streams:
         cur.wait_stream(st)
     cur.synchronize()
@@ -502,7 +503,13 @@ def eval_eq(party: int, k: EqKeyBatch, x):
             _lib.call("fss_dpf_eval", int(party), n, hi - lo, ld, _dev.ptr(seed0[lo:hi]),
                       _dev.ptr(k.scw[:, lo:hi]), _dev.ptr(k.tcw[:, lo:hi]),
                       _dev.ptr(cw_final[lo:hi]), _dev.ptr(xd), _dev.ptr(od), stream)
-    return _run_eval(launch, xt, host, count, dev)
+
+    def host_launch(xh, oh, xs, os_, chunk, sa, sb):
+        with torch.cuda.device(dev):
+            _lib.call("fss_dpf_eval_host", int(party), n, count, ld, _dev.ptr(seed0),
+                      _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(cw_final), xh.data_ptr(),
+                      oh.data_ptr(), _dev.ptr(xs), _dev.ptr(os_), chunk, sa, sb)
+    return _run_eval(launch, xt, host, count, dev, host_launch)
 
 
 def eval_cmp(party: int, k: CmpKeyBatch, x, return_levels: bool = False):
@@ -532,7 +539,14 @@ def eval_cmp(party: int, k: CmpKeyBatch, x, return_levels: bool = False):
                       _dev.ptr(seed0[lo:hi]), _dev.ptr(k.scw[:, lo:hi]), _dev.ptr(k.tcw[:, lo:hi]),
                       _dev.ptr(k.sigma_cw[:, lo:hi]), _dev.ptr(k.leaf_cw[:, lo:hi]), _dev.ptr(xd),
                       _dev.ptr(od), None, stream)
-    return _run_eval(launch, xt, host, count, dev)
+
+    def host_launch(xh, oh, xs, os_, chunk, sa, sb):
+        with torch.cuda.device(dev):
+            _lib.call("fss_dcf_eval_host", int(party), n, int(k.out_bits), count, ld,
+                      _dev.ptr(seed0), _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(k.sigma_cw),
+                      _dev.ptr(k.leaf_cw), xh.data_ptr(), oh.data_ptr(), _dev.ptr(xs),
+                      _dev.ptr(os_), chunk, sa, sb)
+    return _run_eval(launch, xt, host, count, dev, host_launch)
 
 
 # ---------------------------------------------------------------------------
