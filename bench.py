@@ -397,7 +397,9 @@ def run_ours(args, ws, rank, local):
             r1 = fss.eval_cmp(1, k1, x_host)
             return r0, r1
 
-        for _ in range(args.warmup):
+        # warm-up: the first host-pipeline calls also set up pinned staging
+        # blocks and side streams (one-time costs a long-running caller never sees)
+        for _ in range(max(args.warmup, 5)):
             r0, r1 = e2e_step()
         want = (x_host.view(torch.int64) <= alpha.view(torch.int64).cpu()).to(torch.int64)
         assert torch.equal((r0.view(torch.int64) + r1.view(torch.int64)) & 0xFFFFFFFF, want)
@@ -417,7 +419,8 @@ def run_ours(args, ws, rank, local):
             _, q0, q1 = fss.keygen_cmp(N_BITS, rng2, N, device=dev)
             return fss.eval_cmp(0, q0, x_host), fss.eval_cmp(1, q1, x_host)
 
-        e2e_keygen_step()
+        for _ in range(3):   # fills the allocator's cache for two generations of keys
+            e2e_keygen_step()
         ksteps = max(3, args.steps // 4)
         t_kg = timed_host(e2e_keygen_step, ksteps)
         e2e["with_keygen"] = {"value": ws * N * ksteps / t_kg, "unit": "comparisons/s",
