@@ -186,6 +186,17 @@ int fss_beaver_mul(int party, int n_bits, uint64_t count, const void* delta_own,
                    const uint64_t* a, const uint64_t* b, const uint64_t* c, uint64_t* z,
                    void* stream);
 
+/* CUDA IPC for the peer-memory exchange (runtime.PeerTransport): export a
+ * device allocation as an opaque handle (fss_ipc_handle_bytes() bytes), map a
+ * peer process's allocation (peer access enabled lazily), unmap it. Replaces
+ * the byte transport under Session.exchange (runtime.py:228-257) when both
+ * parties run on one node: the eval kernel then loads the peer's masked message
+ * directly (fss_*_eval_masked with m_peer = the mapped pointer). */
+int fss_ipc_handle_bytes(void);
+int fss_ipc_get_handle(const void* dev_ptr, uint8_t* handle);
+int fss_ipc_open_handle(const uint8_t* handle, void** dev_ptr);
+int fss_ipc_close_handle(void* dev_ptr);
+
 /* Diagnostics (not a reference entry point): on-box peak probes used as the
  * roofline denominators of the AES work. Synchronous; runs ~10 ms of probe
  * kernels on the current device. */

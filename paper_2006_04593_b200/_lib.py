@@ -60,6 +60,10 @@ SIGNATURES = {
     "fss_wire_pack": [_int, _int, _u64, _vp, _vp, _vp, _vp],
     "fss_wire_open": [_int, _u64, _vp, _vp, _vp, _vp],
     "fss_probe_peaks": [ctypes.POINTER(Peaks)],
+    "fss_ipc_handle_bytes": [],
+    "fss_ipc_get_handle": [_vp, _vp],
+    "fss_ipc_open_handle": [_vp, ctypes.POINTER(ctypes.c_void_p)],
+    "fss_ipc_close_handle": [_vp],
 }
 _RESTYPE = {"fss_last_error": ctypes.c_char_p, "fss_arnk_elem_bytes": ctypes.c_uint64}
 

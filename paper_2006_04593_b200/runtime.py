@@ -209,6 +209,164 @@ class DistTransport:
         self._closed = True
 
 
+class PeerBuffer:
+    """A peer process's device buffer mapped into this process (CUDA IPC).
+
+    Duck-types the few tensor methods the share layer uses on an exchanged
+    payload (dtype, numel, data_ptr, flat slicing), so the evaluation kernels
+    read the peer's masked message in place: over NVLink / NVSwitch when the
+    peer is another GPU, from the same HBM when both processes share one."""
+
+    is_cuda = True
+
+    def __init__(self, ptr: int, numel: int, dtype: torch.dtype, device: torch.device):
+        self._ptr, self._numel, self.dtype, self.device = ptr, numel, dtype, device
+
+    @property
+    def shape(self):
+        return (self._numel,)
+
+    def numel(self) -> int:
+        return self._numel
+
+    def element_size(self) -> int:
+        return torch.empty(0, dtype=self.dtype).element_size()
+
+    def data_ptr(self) -> int:
+        return self._ptr
+
+    def to(self, device=None, *args, **kwargs):
+        if device is not None and torch.device(device) != self.device:
+            raise ValueError("a mapped peer buffer is only addressable from its own device")
+        return self
+
+    def reshape(self, *shape):
+        if shape not in ((-1,), (self._numel,), ((-1,),), ((self._numel,),)):
+            raise ValueError("mapped peer buffers are flat")
+        return self
+
+    def contiguous(self):
+        return self
+
+    def __getitem__(self, idx):
+        if not isinstance(idx, slice) or idx.step not in (None, 1):
+            raise TypeError("mapped peer buffers support contiguous slices only")
+        lo, hi, _ = idx.indices(self._numel)
+        hi = max(hi, lo)
+        return PeerBuffer(self._ptr + lo * self.element_size(), hi - lo, self.dtype, self.device)
+
+    def __repr__(self):
+        return f"PeerBuffer(ptr=0x{self._ptr:x}, numel={self._numel}, dtype={self.dtype})"
+
+
+class PeerTransport:
+    """Same-node transport over CUDA IPC peer memory (one party per process).
+
+    Each process owns two message slots in its HBM and maps the peer's two
+    slots. ``exchange`` writes our wire-packed payload into our slot, makes it
+    visible (stream sync), meets the peer at a barrier and returns the peer's
+    slot as a :class:`PeerBuffer`: no copy of the peer's message is made -- the
+    consuming kernel (e.g. fss_dcf_eval_masked) loads it directly over NVLink.
+    Slots alternate per round, and every round starts with a stream sync +
+    barrier, so a slot is only rewritten after the peer finished reading it.
+    The small frame header (tag, dtype, size) goes through torch.distributed
+    exactly as in :class:`DistTransport` and sizes grow both sides' slots in
+    lock-step."""
+
+    def __init__(self, peer: int, group=None, device=None, capacity: int = 1 << 20):
+        import torch.distributed as dist
+        from . import _lib
+        self._dist, self._lib = dist, _lib
+        self.peer, self.group = peer, group
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self._hdr_device = (self.device if dist.get_backend(group) == "nccl"
+                            else torch.device("cpu"))
+        self._slots, self._peer_ptrs, self._cap, self._round = [], [], 0, 0
+        self._closed = False
+        self._grow(capacity)
+
+    def _swap(self, t: torch.Tensor) -> torch.Tensor:
+        dist = self._dist
+        t = t.to(self._hdr_device)
+        out = torch.empty_like(t)
+        ops = [dist.P2POp(dist.isend, t, self.peer, self.group),
+               dist.P2POp(dist.irecv, out, self.peer, self.group)]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        return out.cpu()
+
+    def _grow(self, nbytes: int):
+        import ctypes
+        lib = self._lib
+        for p in self._peer_ptrs:
+            lib.call("fss_ipc_close_handle", ctypes.c_void_p(p))
+        torch.cuda.current_stream(self.device).synchronize()
+        cap = max(int(nbytes), 1 << 12)
+        self._slots = [torch.empty(cap, dtype=torch.uint8, device=self.device) for _ in range(2)]
+        hb = lib.load().fss_ipc_handle_bytes()
+        mine = torch.zeros((2, hb), dtype=torch.uint8)
+        for i, slot in enumerate(self._slots):
+            buf = (ctypes.c_uint8 * hb)()
+            lib.call("fss_ipc_get_handle", ctypes.c_void_p(slot.data_ptr()), buf)
+            mine[i] = torch.tensor(list(buf), dtype=torch.uint8)
+        theirs = self._swap(mine)
+        self._peer_ptrs = []
+        for i in range(2):
+            raw = (ctypes.c_uint8 * hb)(*theirs[i].tolist())
+            ptr = ctypes.c_void_p()
+            with torch.cuda.device(self.device):
+                lib.call("fss_ipc_open_handle", raw, ctypes.byref(ptr))
+            self._peer_ptrs.append(ptr.value)
+        self._cap = cap
+
+    def exchange_frames(self, frame: Frame) -> Frame:
+        if self._closed:
+            raise SessionAbort("transport closed")
+        p = frame.payload.contiguous()
+        nbytes = p.numel() * p.element_size()
+        hdr = torch.tensor([frame.tag, _DTYPE_CODE[p.dtype], p.numel(), nbytes], dtype=torch.int64)
+        tag, code, numel, peer_bytes = (int(v) for v in self._swap(hdr).tolist())
+        if tag == FRAME_ABORT:
+            raise SessionAbort("peer aborted")
+        if code < 0 or code >= len(_DTYPES):
+            raise SessionAbort("corrupt frame header")
+        need = max(nbytes, peer_bytes)
+        if need > self._cap:                    # both sides see both sizes: lock-step growth
+            self._grow(2 * need)
+        slot = self._round & 1
+        self._round += 1
+        if nbytes:
+            self._slots[slot][:nbytes].copy_(p.reshape(-1).view(torch.uint8))
+        # our message is in HBM and every earlier read of the peer's slots is done
+        torch.cuda.current_stream(self.device).synchronize()
+        self._dist.barrier(group=self.group) if self.group is not None else self._dist.barrier()
+        return Frame(tag, PeerBuffer(self._peer_ptrs[slot], numel, _DTYPES[code], self.device))
+
+    def send_abort(self):
+        self._aborted = True
+        try:
+            self._swap(torch.tensor([FRAME_ABORT, 0, 0, 0], dtype=torch.int64))
+        except Exception:  # noqa: BLE001
+            pass
+
+    def close(self):
+        if not self._closed:
+            import ctypes
+            self._closed = True
+            torch.cuda.current_stream(self.device).synchronize()
+            if not getattr(self, "_aborted", False):
+                # the peer may still be reading our slots: leave together
+                self._dist.barrier(group=self.group) if self.group is not None \
+                    else self._dist.barrier()
+            for p in self._peer_ptrs:
+                try:
+                    self._lib.call("fss_ipc_close_handle", ctypes.c_void_p(p))
+                except RuntimeError:
+                    pass
+            self._peer_ptrs = []
+
+
 # ---------------------------------------------------------------------------
 # Session
 # ---------------------------------------------------------------------------
@@ -235,7 +393,7 @@ class Session:
             raise ValueError(f"unknown frame tag {tag}")
         frame = Frame(tag, payload)
         try:
-            if isinstance(self.transport, DistTransport):
+            if isinstance(self.transport, (DistTransport, PeerTransport)):
                 peer = self.transport.exchange_frames(frame)
             else:
                 self.transport.send(frame)
@@ -255,7 +413,7 @@ class Session:
     def abort(self, reason: str = ""):
         if self.open:
             try:
-                if isinstance(self.transport, DistTransport):
+                if isinstance(self.transport, (DistTransport, PeerTransport)):
                     self.transport.send_abort()
                 else:
                     self.transport.send(Frame(FRAME_ABORT, torch.empty(0, dtype=torch.uint8)))
@@ -327,3 +485,9 @@ def run_local_pair(program0, program1=None, device=None):
 def run_dist_party(party: int, peer: int, program, group=None, device=None):
     """This process plays ``party`` against the process of global rank ``peer``."""
     return run_session(party, DistTransport(peer, group, device), program)
+
+
+def run_peer_party(party: int, peer: int, program, group=None, device=None, capacity=1 << 20):
+    """As run_dist_party, but the masked messages are read in place from the
+    peer's HBM through CUDA IPC (:class:`PeerTransport`)."""
+    return run_session(party, PeerTransport(peer, group, device, capacity), program)

@@ -1,0 +1,46 @@
+"""Small workload that launches every kernel of libariann_fss.so once or twice,
+for compute-sanitizer (memcheck / racecheck / initcheck / synccheck)."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2006_04593_b200 import _dev, _lib, dealer, fss, nn_ops, prg, runtime  # noqa: E402
+from paper_2006_04593_b200.sharing import encode_fixed, share  # noqa: E402
+
+torch.cuda.set_device(0)
+rng = np.random.default_rng(1)
+for n, N in ((32, 3000), (12, 513), (63, 77)):
+    a, k0, k1 = fss.keygen_cmp(n, rng, N)
+    x = rng.integers(0, 1 << n, N, dtype=np.uint64)
+    fss.eval_cmp(0, k0, x)
+    fss.eval_cmp(1, k1, x, return_levels=True)
+    a, e0, e1 = fss.keygen_eq(n, rng, N)
+    fss.eval_eq(0, e0, x)
+    if n <= 32:
+        fss.unpack_keys(fss.deserialize_keys(fss.serialize_keys(fss.pack_keys(k0, k1))))
+        fss.unpack_keys(fss.deserialize_keys(fss.serialize_keys(fss.pack_keys(e0, e1))))
+fss.keygen_eq(64, rng, 100)
+fss.keygen_cmp(16, rng, 64, out_bits=40)
+prg.expand(rng.integers(0, 256, (1000, 16), dtype=np.uint8), 3)
+seeds = torch.randint(0, 256, (1024, 16), dtype=torch.uint8, device="cuda")
+out = torch.empty((1024, 48), dtype=torch.uint8, device="cuda")
+_lib.call("fss_aes_mmo_expand_bitsliced", _dev.ptr(seeds), 1024, 3, _dev.ptr(out),
+          ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+prg.mask_stream(bytes(range(16)), 3, 1001, 32)
+xs = share(encode_fixed(rng.uniform(-10, 10, (2, 8, 8)), 3, 32), rng, precision=3)
+d = dealer.make_dealer(32, seed=2)
+runtime.run_local_pair(lambda s: nn_ops.maxpool(s, xs[s.party], 2,
+                                                d.for_party(s.party).maxpool(8, 2, 2, planes=2), 2))
+runtime.run_local_pair(lambda s: nn_ops.maxpool_k2(s, xs[s.party],
+                                                   d.for_party(s.party).maxpool_k2(8, planes=2)))
+# host pipeline with a small chunk so several chunks run
+fss.PIPELINE_MIN, fss.PIPELINE_CHUNK = 1 << 10, 1 << 9
+a, k0, k1 = fss.keygen_cmp(32, rng, 3000)
+xh = torch.from_numpy(rng.integers(0, 1 << 32, 3000, dtype=np.uint64).view(np.int64)).pin_memory()
+fss.eval_cmp(0, k0, xh.view(torch.uint64))
+torch.cuda.synchronize()
+print("sanitize workload done")

@@ -1,4 +1,6 @@
-"""The two parties as two processes (one per rank) over runtime.DistTransport.
+"""The two parties as two processes (one per rank) over runtime.DistTransport
+and over runtime.PeerTransport (CUDA IPC: the eval kernel reads the peer's
+masked message in place; capacity is set small so the slots grow mid-run).
 
 On a multi-GPU box each rank owns a GPU and the masked message travels over
 NCCL; this test runs both ranks on cuda:0 with the gloo transport (payloads
@@ -31,7 +33,7 @@ def _port():
         return s.getsockname()[1]
 
 
-def _worker(rank, port, name, q):
+def _worker(rank, port, name, q, transport="dist"):
     import torch.distributed as dist
 
     from paper_2006_04593_b200 import dealer, fss, nn_ops, runtime
@@ -56,21 +58,26 @@ def _worker(rank, port, name, q):
             return fss.sign_protocol(session, AdditiveShare(session.party, xs[session.party].values, 0),
                                      keys)
         # the dealer must produce both halves in order in each process
-        res, ledger = runtime.run_dist_party(rank, 1 - rank, prog, device="cpu")
+        if transport == "peer":
+            # masked messages read in place from the peer process's HBM (CUDA IPC)
+            res, ledger = runtime.run_peer_party(rank, 1 - rank, prog, capacity=256)
+        else:
+            res, ledger = runtime.run_dist_party(rank, 1 - rank, prog, device="cpu")
         vals = res.values.numpy().astype("<u8")
         q.put((rank, vals.tobytes(), ledger.total_rounds(), ledger.total_bytes_sent()))
     finally:
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("transport", ["dist", "peer"])
 @pytest.mark.parametrize("name", ["relu_small", "compare_n32"])
-def test_two_process_protocol_matches_reference(name):
+def test_two_process_protocol_matches_reference(name, transport):
     with open(os.path.join(GOLDEN, "protocols.json")) as fh:
         c = json.load(fh)["cases"][name]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, port, name, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, port, name, q, transport)) for r in range(2)]
     for p in procs:
         p.start()
     got = dict((r, (v, rounds, nb)) for r, v, rounds, nb in (q.get(timeout=300) for _ in range(2)))
