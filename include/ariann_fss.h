@@ -193,6 +193,9 @@ int fss_beaver_mul(int party, int n_bits, uint64_t count, const void* delta_own,
  * parties run on one node: the eval kernel then loads the peer's masked message
  * directly (fss_*_eval_masked with m_peer = the mapped pointer). */
 int fss_ipc_handle_bytes(void);
+int fss_ipc_alloc(uint64_t nbytes, void** dev_ptr);   /* whole allocation: exportable */
+int fss_ipc_free(void* dev_ptr);
+int fss_memcpy_d2d(void* dst, const void* src, uint64_t nbytes, void* stream);
 int fss_ipc_get_handle(const void* dev_ptr, uint8_t* handle);
 int fss_ipc_open_handle(const uint8_t* handle, void** dev_ptr);
 int fss_ipc_close_handle(void* dev_ptr);

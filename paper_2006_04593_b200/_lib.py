@@ -61,6 +61,9 @@ SIGNATURES = {
     "fss_wire_open": [_int, _u64, _vp, _vp, _vp, _vp],
     "fss_probe_peaks": [ctypes.POINTER(Peaks)],
     "fss_ipc_handle_bytes": [],
+    "fss_ipc_alloc": [_u64, ctypes.POINTER(ctypes.c_void_p)],
+    "fss_ipc_free": [_vp],
+    "fss_memcpy_d2d": [_vp, _vp, _u64, _vp],
     "fss_ipc_get_handle": [_vp, _vp],
     "fss_ipc_open_handle": [_vp, ctypes.POINTER(ctypes.c_void_p)],
     "fss_ipc_close_handle": [_vp],

@@ -13,6 +13,29 @@ extern "C" {
 
 int fss_ipc_handle_bytes(void) { return (int)sizeof(cudaIpcMemHandle_t); }
 
+// Exported buffers are whole cudaMalloc allocations: an IPC handle names the
+// allocation BASE, so a sub-allocation of a caching allocator would map at the
+// wrong address in the peer.
+int fss_ipc_alloc(uint64_t nbytes, void** dev_ptr) {
+    const cudaError_t err = cudaMalloc(dev_ptr, nbytes);
+    if (err != cudaSuccess) return fssb::set_error(FSS_ECUDA, cudaGetErrorString(err));
+    return FSS_OK;
+}
+
+int fss_ipc_free(void* dev_ptr) {
+    const cudaError_t err = cudaFree(dev_ptr);
+    if (err != cudaSuccess) return fssb::set_error(FSS_ECUDA, cudaGetErrorString(err));
+    return FSS_OK;
+}
+
+int fss_memcpy_d2d(void* dst, const void* src, uint64_t nbytes, void* stream) {
+    if (!nbytes) return FSS_OK;
+    const cudaError_t err =
+        cudaMemcpyAsync(dst, src, nbytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+    if (err != cudaSuccess) return fssb::set_error(FSS_ECUDA, cudaGetErrorString(err));
+    return FSS_OK;
+}
+
 int fss_ipc_get_handle(const void* dev_ptr, uint8_t* handle) {
     cudaIpcMemHandle_t h;
     const cudaError_t err = cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr));

@@ -299,26 +299,43 @@ class PeerTransport:
     def _grow(self, nbytes: int):
         import ctypes
         lib = self._lib
-        for p in self._peer_ptrs:
-            lib.call("fss_ipc_close_handle", ctypes.c_void_p(p))
         torch.cuda.current_stream(self.device).synchronize()
+        self._release()
         cap = max(int(nbytes), 1 << 12)
-        self._slots = [torch.empty(cap, dtype=torch.uint8, device=self.device) for _ in range(2)]
         hb = lib.load().fss_ipc_handle_bytes()
         mine = torch.zeros((2, hb), dtype=torch.uint8)
-        for i, slot in enumerate(self._slots):
-            buf = (ctypes.c_uint8 * hb)()
-            lib.call("fss_ipc_get_handle", ctypes.c_void_p(slot.data_ptr()), buf)
-            mine[i] = torch.tensor(list(buf), dtype=torch.uint8)
+        with torch.cuda.device(self.device):
+            for i in range(2):
+                ptr = ctypes.c_void_p()
+                lib.call("fss_ipc_alloc", cap, ctypes.byref(ptr))
+                self._slots.append(ptr.value)
+                buf = (ctypes.c_uint8 * hb)()
+                lib.call("fss_ipc_get_handle", ptr, buf)
+                mine[i] = torch.tensor(list(buf), dtype=torch.uint8)
         theirs = self._swap(mine)
-        self._peer_ptrs = []
-        for i in range(2):
-            raw = (ctypes.c_uint8 * hb)(*theirs[i].tolist())
-            ptr = ctypes.c_void_p()
-            with torch.cuda.device(self.device):
+        with torch.cuda.device(self.device):
+            for i in range(2):
+                raw = (ctypes.c_uint8 * hb)(*theirs[i].tolist())
+                ptr = ctypes.c_void_p()
                 lib.call("fss_ipc_open_handle", raw, ctypes.byref(ptr))
-            self._peer_ptrs.append(ptr.value)
+                self._peer_ptrs.append(ptr.value)
         self._cap = cap
+
+    def _release(self):
+        """Unmap the peer's slots and free ours (callers synchronise first)."""
+        import ctypes
+        with torch.cuda.device(self.device):
+            for p in self._peer_ptrs:
+                try:
+                    self._lib.call("fss_ipc_close_handle", ctypes.c_void_p(p))
+                except RuntimeError:
+                    pass
+            for p in self._slots:
+                try:
+                    self._lib.call("fss_ipc_free", ctypes.c_void_p(p))
+                except RuntimeError:
+                    pass
+        self._peer_ptrs, self._slots = [], []
 
     def exchange_frames(self, frame: Frame) -> Frame:
         if self._closed:
@@ -333,11 +350,16 @@ class PeerTransport:
             raise SessionAbort("corrupt frame header")
         need = max(nbytes, peer_bytes)
         if need > self._cap:                    # both sides see both sizes: lock-step growth
+            self._dist.barrier(group=self.group) if self.group is not None \
+                else self._dist.barrier()       # the peer stopped reading the old slots
             self._grow(2 * need)
         slot = self._round & 1
         self._round += 1
-        if nbytes:
-            self._slots[slot][:nbytes].copy_(p.reshape(-1).view(torch.uint8))
+        import ctypes
+        with torch.cuda.device(self.device):
+            self._lib.call("fss_memcpy_d2d", ctypes.c_void_p(self._slots[slot]),
+                           ctypes.c_void_p(p.data_ptr() if nbytes else 0), nbytes,
+                           ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream))
         # our message is in HBM and every earlier read of the peer's slots is done
         torch.cuda.current_stream(self.device).synchronize()
         self._dist.barrier(group=self.group) if self.group is not None else self._dist.barrier()
@@ -359,12 +381,7 @@ class PeerTransport:
                 # the peer may still be reading our slots: leave together
                 self._dist.barrier(group=self.group) if self.group is not None \
                     else self._dist.barrier()
-            for p in self._peer_ptrs:
-                try:
-                    self._lib.call("fss_ipc_close_handle", ctypes.c_void_p(p))
-                except RuntimeError:
-                    pass
-            self._peer_ptrs = []
+            self._release()
 
 
 # ---------------------------------------------------------------------------
