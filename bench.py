@@ -272,6 +272,42 @@ def measure_exchange(dev, xdev, rank, ws, N, barrier, max_over_ranks):
             "pairs": ws // 2, "note": "wall clock incl. the 24-byte frame header round trip"}
 
 
+def measure_pair_protocol(dev, xdev, rank, barrier, max_over_ranks, M=1 << 22, reps=5):
+    """The online sign test with the two parties on two GPUs: rank r plays party
+    r % 2 against rank r ^ 1 (mask -> exchange -> DCF eval, one round), once
+    with the message over NCCL (DistTransport) and once read in place from the
+    peer's HBM by the eval kernel (PeerTransport, CUDA IPC over NVLink).
+    Max over ranks of the wall time per call."""
+    import numpy as np
+    import torch
+
+    from paper_2006_04593_b200 import dealer, fss, runtime
+    from paper_2006_04593_b200.sharing import AdditiveShare, encode_fixed, share
+
+    party, peer, pair = rank % 2, rank ^ 1, rank // 2
+    rng = np.random.default_rng(88 + pair)
+    xs = share(encode_fixed(rng.uniform(-100, 100, M), 3, 32, device=dev), rng, precision=3)
+    y = AdditiveShare(party, xs[party].values, 0)
+    out = {"elements_per_pair": M}
+    for name, make in (("nccl", lambda: runtime.DistTransport(peer, device=xdev)),
+                       ("peer_memory", lambda: runtime.PeerTransport(peer, device=dev,
+                                                                     capacity=8 * M))):
+        keys = dealer.make_dealer(32, seed=77 + pair).for_party(party).cmp_keys(M * (reps + 1))
+        sess = runtime.Session(party, make())
+        fss.sign_protocol(sess, y, keys)          # warm-up
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            r = fss.sign_protocol(sess, y, keys)
+        torch.cuda.synchronize()
+        t = max_over_ranks((time.perf_counter() - t0) / reps)
+        sess.close()
+        out[name] = {"ms_per_call": t * 1e3, "comparisons_per_s_per_pair": M / t}
+        del keys, r
+    return out
+
+
 def run_ours(args, ws, rank, local):
     import numpy as np
     import torch
@@ -365,6 +401,8 @@ def run_ours(args, ws, rank, local):
         secondary = dict(secondary or {})
         secondary["nccl_masked_exchange"] = measure_exchange(dev, xdev, rank, ws, N, barrier,
                                                              max_over_ranks)
+        secondary["two_gpu_sign_protocol"] = measure_pair_protocol(dev, xdev, rank, barrier,
+                                                                   max_over_ranks)
     del out0, out1, rec
 
     # ---- e2e through the public API with host buffers ----------------------

@@ -38,3 +38,6 @@ def test_two_rank_bench_contract():
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] == 6
     ex = d["secondary"]["nccl_masked_exchange"]
     assert ex["bytes_each_way_per_rank"] == 4 << 18 and ex["pairs"] == 1
+    pp = d["secondary"]["two_gpu_sign_protocol"]
+    assert pp["nccl"]["comparisons_per_s_per_pair"] > 0
+    assert pp["peer_memory"]["comparisons_per_s_per_pair"] > 0
