@@ -126,17 +126,21 @@ int fss_dcf_eval_masked(int party, int n, int out_bits, uint64_t count, uint64_t
  * of the drop-in): [0, count) is streamed in `chunk`-element pieces over two
  * streams -- cudaMemcpyAsync of x_host (pinned) into x_dev, the eval kernel,
  * cudaMemcpyAsync of the shares into out_host (pinned) -- so copies overlap
- * kernels. x_dev / out_dev are caller scratch of 2 * chunk words each. Returns
- * once enqueued; the caller synchronises stream_a and stream_b. */
+ * kernels. x_dev / out_dev are caller scratch of 2 * chunk words each.
+ * stage == NULL: x_host / out_host are pinned; returns once enqueued and the
+ * caller synchronises stream_a and stream_b. stage != NULL (4 * chunk pinned
+ * words): x_host / out_host may be pageable (numpy arrays); chunks are staged
+ * by host memcpy overlapping the GPU work, and the call returns when out_host
+ * is complete. */
 int fss_dcf_eval_host(int party, int n, int out_bits, uint64_t count, uint64_t ld,
                       const uint8_t* seed0, const uint8_t* scw, const uint8_t* tcw,
                       const uint64_t* sigma_cw, const uint64_t* leaf_cw, const uint64_t* x_host,
                       uint64_t* out_host, uint64_t* x_dev, uint64_t* out_dev, uint64_t chunk,
-                      void* stream_a, void* stream_b);
+                      uint64_t* stage, void* stream_a, void* stream_b);
 int fss_dpf_eval_host(int party, int n, uint64_t count, uint64_t ld, const uint8_t* seed0,
                       const uint8_t* scw, const uint8_t* tcw, const uint64_t* cw_final,
                       const uint64_t* x_host, uint64_t* out_host, uint64_t* x_dev, uint64_t* out_dev,
-                      uint64_t chunk, void* stream_a, void* stream_b);
+                      uint64_t chunk, uint64_t* stage, void* stream_a, void* stream_b);
 
 /* ARNK per-party payloads (LAYOUT.md:48-71; fss._pack_eq/_pack_cmp fss.py:540-583,
  * _unpack_eq/_unpack_cmp fss.py:553-602). kind 0 = equality, 1 = comparison.

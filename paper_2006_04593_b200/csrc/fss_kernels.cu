@@ -657,12 +657,11 @@ struct HostPipe {
     uint64_t* out_dev;
     uint64_t chunk;
     cudaStream_t st[2];
+    uint64_t* stage;  // NULL: host buffers are pinned; else 4 * chunk pinned words
 };
 
 template <typename Launch>
-int run_host_pipe(const HostPipe& hp, uint64_t count, Launch launch) {
-    if (!hp.x_host || !hp.out_host || !hp.x_dev || !hp.out_dev || hp.chunk == 0)
-        return set_err(kEinval, "pipelined eval needs host/device buffers and a chunk size%s");
+int run_host_pipe_pinned(const HostPipe& hp, uint64_t count, Launch launch) {
     for (uint64_t i = 0, lo = 0; lo < count; i++, lo += hp.chunk) {
         const uint64_t m = count - lo < hp.chunk ? count - lo : hp.chunk;
         const int slot = (int)(i & 1);
@@ -676,6 +675,70 @@ int run_host_pipe(const HostPipe& hp, uint64_t count, Launch launch) {
         if (err != cudaSuccess) return set_err(kEcuda, "D2H: %s", cudaGetErrorString(err));
     }
     return kOk;
+}
+
+// Pageable host buffers (e.g. numpy arrays): chunks are staged through pinned
+// slots by host memcpy, which overlaps the other slot's copies and kernel.
+// Returns when every share is in out_host.
+template <typename Launch>
+int run_host_pipe_staged(const HostPipe& hp, uint64_t count, Launch launch) {
+    cudaEvent_t h2d[2], d2h[2];
+    for (int k = 0; k < 2; k++) {
+        cudaEventCreateWithFlags(&h2d[k], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&d2h[k], cudaEventDisableTiming);
+    }
+    uint64_t* sin[2] = {hp.stage, hp.stage + hp.chunk};
+    uint64_t* sout[2] = {hp.stage + 2 * hp.chunk, hp.stage + 3 * hp.chunk};
+    bool in_busy[2] = {false, false}, out_busy[2] = {false, false};
+    uint64_t out_lo[2] = {0, 0}, out_m[2] = {0, 0};
+    int rc = kOk;
+    auto drain = [&](int k) {
+        if (!out_busy[k]) return;
+        cudaEventSynchronize(d2h[k]);
+        memcpy(hp.out_host + out_lo[k], sout[k], out_m[k] * 8);
+        out_busy[k] = false;
+    };
+    for (uint64_t i = 0, lo = 0; lo < count && rc == kOk; i++, lo += hp.chunk) {
+        const uint64_t m = count - lo < hp.chunk ? count - lo : hp.chunk;
+        const int slot = (int)(i & 1);
+        cudaStream_t s = hp.st[slot];
+        uint64_t* xd = hp.x_dev + slot * hp.chunk;
+        uint64_t* od = hp.out_dev + slot * hp.chunk;
+        if (in_busy[slot]) cudaEventSynchronize(h2d[slot]);   // staging slot free again
+        memcpy(sin[slot], hp.x_host + lo, m * 8);
+        cudaError_t err = cudaMemcpyAsync(xd, sin[slot], m * 8, cudaMemcpyHostToDevice, s);
+        if (err != cudaSuccess) { rc = set_err(kEcuda, "H2D: %s", cudaGetErrorString(err)); break; }
+        cudaEventRecord(h2d[slot], s);
+        in_busy[slot] = true;
+        if ((rc = launch(lo, m, xd, od, s)) != kOk) break;
+        err = cudaMemcpyAsync(sout[slot], od, m * 8, cudaMemcpyDeviceToHost, s);
+        if (err != cudaSuccess) { rc = set_err(kEcuda, "D2H: %s", cudaGetErrorString(err)); break; }
+        cudaEventRecord(d2h[slot], s);
+        drain(slot ^ 1);                                      // previous chunk's shares
+        out_busy[slot] = true;
+        out_lo[slot] = lo;
+        out_m[slot] = m;
+    }
+    if (rc == kOk) {
+        const int first = out_busy[0] && out_busy[1] ? (out_lo[0] < out_lo[1] ? 0 : 1) : (out_busy[0] ? 0 : 1);
+        drain(first);
+        drain(first ^ 1);
+    } else {
+        cudaStreamSynchronize(hp.st[0]);
+        cudaStreamSynchronize(hp.st[1]);
+    }
+    for (int k = 0; k < 2; k++) {
+        cudaEventDestroy(h2d[k]);
+        cudaEventDestroy(d2h[k]);
+    }
+    return rc;
+}
+
+template <typename Launch>
+int run_host_pipe(const HostPipe& hp, uint64_t count, Launch launch) {
+    if (!hp.x_host || !hp.out_host || !hp.x_dev || !hp.out_dev || hp.chunk == 0)
+        return set_err(kEinval, "pipelined eval needs host/device buffers and a chunk size%s");
+    return hp.stage ? run_host_pipe_staged(hp, count, launch) : run_host_pipe_pinned(hp, count, launch);
 }
 
 }  // namespace
@@ -708,9 +771,9 @@ int fss_dcf_eval_host(int party, int n, int out_bits, uint64_t count, uint64_t l
                       const uint8_t* seed0, const uint8_t* scw, const uint8_t* tcw,
                       const uint64_t* sigma_cw, const uint64_t* leaf_cw, const uint64_t* x_host,
                       uint64_t* out_host, uint64_t* x_dev, uint64_t* out_dev, uint64_t chunk,
-                      void* stream_a, void* stream_b) {
+                      uint64_t* stage, void* stream_a, void* stream_b) {
     const HostPipe hp{x_host, out_host, x_dev, out_dev, chunk,
-                      {(cudaStream_t)stream_a, (cudaStream_t)stream_b}};
+                      {(cudaStream_t)stream_a, (cudaStream_t)stream_b}, stage};
     return run_host_pipe(hp, count, [&](uint64_t lo, uint64_t m, const uint64_t* xd, uint64_t* od,
                                         cudaStream_t s) {
         return launch_dcf_eval(party, n, out_bits, m, ld, seed0 + 16 * lo, scw + 16 * lo, tcw + lo,
@@ -721,9 +784,9 @@ int fss_dcf_eval_host(int party, int n, int out_bits, uint64_t count, uint64_t l
 int fss_dpf_eval_host(int party, int n, uint64_t count, uint64_t ld, const uint8_t* seed0,
                       const uint8_t* scw, const uint8_t* tcw, const uint64_t* cw_final,
                       const uint64_t* x_host, uint64_t* out_host, uint64_t* x_dev, uint64_t* out_dev,
-                      uint64_t chunk, void* stream_a, void* stream_b) {
+                      uint64_t chunk, uint64_t* stage, void* stream_a, void* stream_b) {
     const HostPipe hp{x_host, out_host, x_dev, out_dev, chunk,
-                      {(cudaStream_t)stream_a, (cudaStream_t)stream_b}};
+                      {(cudaStream_t)stream_a, (cudaStream_t)stream_b}, stage};
     return run_host_pipe(hp, count, [&](uint64_t lo, uint64_t m, const uint64_t* xd, uint64_t* od,
                                         cudaStream_t s) {
         return launch_dpf_eval(party, n, m, ld, seed0 + 16 * lo, scw + 16 * lo, tcw + lo,

@@ -453,29 +453,37 @@ PIPELINE_CHUNK = 1 << 20
 def _run_eval(launch, xt, host, count: int, dev, host_launch=None):
     """Run the evaluation over [0, count).
 
-    Device (or numpy) input: ``launch(lo, hi, x_dev, out_dev, stream)`` once on
-    the current stream. Pinned host torch input: ``host_launch(x_host, out_host,
-    x_scratch, out_scratch, chunk, stream_a, stream_b)`` -- one native call
-    (fss_*_eval_host) that streams chunks over two CUDA streams so the H2D copy,
-    the kernel and the D2H copy of consecutive chunks overlap; returns a pinned
-    host tensor."""
-    if host != "torch_pinned" or count < PIPELINE_MIN or host_launch is None:
-        if host == "torch_pinned":
-            xt = xt.to(dev, non_blocking=True)
+    Device input: ``launch(lo, hi, x_dev, out_dev, stream)`` once on the current
+    stream. Host input of at least PIPELINE_MIN elements: ``host_launch(x_ptr,
+    out_ptr, x_scratch, out_scratch, chunk, stage_ptr, stream_a, stream_b)`` --
+    one native call (fss_*_eval_host) streaming chunks over two CUDA streams so
+    the H2D copy, the kernel and the D2H copy of consecutive chunks overlap.
+    Pinned torch input returns a pinned host tensor; numpy input (pageable) is
+    staged through pinned slots inside the call and returns a numpy array."""
+    big = count >= PIPELINE_MIN and host_launch is not None
+    if not big or host not in ("torch_pinned", "numpy"):
+        if host in ("torch_pinned", "numpy"):
+            xt = (torch.from_numpy(xt) if host == "numpy" else xt).to(dev, non_blocking=True)
         out = torch.empty(count, dtype=torch.uint64, device=dev)
         launch(0, count, xt, out, _dev.stream_handle(dev))
-        return _result(out, "torch" if host == "torch_pinned" else host)
+        return _result(out, {"torch_pinned": "torch", "numpy": True}.get(host, host))
     chunk = PIPELINE_CHUNK
-    out_host = torch.empty(count, dtype=torch.uint64, pin_memory=True)
     cur = torch.cuda.current_stream(dev)
-    # scratch on the current stream; the side streams wait for it and the
+    # device scratch on the current stream; the side streams wait for it and the
     # current stream waits for them, so the allocator cannot recycle it early
     scratch = torch.empty((2, 2 * chunk), dtype=torch.uint64, device=dev)
     streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
     for st in streams:
         st.wait_stream(cur)
-    host_launch(xt, out_host, scratch[0], scratch[1], chunk, streams[0].cuda_stream,
-                streams[1].cuda_stream)
+    if host == "torch_pinned":
+        out_host = torch.empty(count, dtype=torch.uint64, pin_memory=True)
+        host_launch(xt.data_ptr(), out_host.data_ptr(), scratch[0], scratch[1], chunk, None,
+                    streams[0].cuda_stream, streams[1].cuda_stream)
+    else:
+        out_host = np.empty(count, dtype=np.uint64)
+        stage = torch.empty(4 * chunk, dtype=torch.uint64, pin_memory=True)
+        host_launch(xt.ctypes.data, out_host.ctypes.data, scratch[0], scratch[1], chunk,
+                    stage.data_ptr(), streams[0].cuda_stream, streams[1].cuda_stream)
     for st in streams:
         cur.wait_stream(st)
     cur.synchronize()
@@ -483,10 +491,14 @@ def _run_eval(launch, xt, host, count: int, dev, host_launch=None):
 
 
 def _prep_x(x, count: int, n: int, dev):
-    """_broadcast_x plus the pinned-host fast path (no upload here)."""
+    """_broadcast_x plus the host fast paths (no upload here; the kernels reduce
+    x mod 2^n themselves)."""
     if isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned() and x.numel() == count \
             and x.dtype in (torch.uint64, torch.int64):
         return x.reshape(-1).contiguous(), "torch_pinned"
+    if isinstance(x, np.ndarray) and x.size == count and count >= PIPELINE_MIN \
+            and x.dtype in (np.uint64, np.int64):
+        return np.ascontiguousarray(x.reshape(-1)).view(np.uint64), "numpy"
     return _broadcast_x(x, count, n, dev)
 
 
@@ -504,11 +516,11 @@ def eval_eq(party: int, k: EqKeyBatch, x):
                       _dev.ptr(k.scw[:, lo:hi]), _dev.ptr(k.tcw[:, lo:hi]),
                       _dev.ptr(cw_final[lo:hi]), _dev.ptr(xd), _dev.ptr(od), stream)
 
-    def host_launch(xh, oh, xs, os_, chunk, sa, sb):
+    def host_launch(xh, oh, xs, os_, chunk, stage, sa, sb):
         with torch.cuda.device(dev):
             _lib.call("fss_dpf_eval_host", int(party), n, count, ld, _dev.ptr(seed0),
-                      _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(cw_final), xh.data_ptr(),
-                      oh.data_ptr(), _dev.ptr(xs), _dev.ptr(os_), chunk, sa, sb)
+                      _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(cw_final), xh, oh,
+                      _dev.ptr(xs), _dev.ptr(os_), chunk, stage, sa, sb)
     return _run_eval(launch, xt, host, count, dev, host_launch)
 
 
@@ -525,6 +537,8 @@ def eval_cmp(party: int, k: CmpKeyBatch, x, return_levels: bool = False):
     if return_levels:
         if host == "torch_pinned":
             xt, host = xt.to(dev), "torch"
+        elif host == "numpy":
+            xt, host = torch.from_numpy(xt).to(dev), True
         out = torch.empty(count, dtype=torch.uint64, device=dev)
         levels = torch.empty((n + 1, count), dtype=torch.uint64, device=dev)
         with torch.cuda.device(dev):
@@ -540,12 +554,12 @@ def eval_cmp(party: int, k: CmpKeyBatch, x, return_levels: bool = False):
                       _dev.ptr(k.sigma_cw[:, lo:hi]), _dev.ptr(k.leaf_cw[:, lo:hi]), _dev.ptr(xd),
                       _dev.ptr(od), None, stream)
 
-    def host_launch(xh, oh, xs, os_, chunk, sa, sb):
+    def host_launch(xh, oh, xs, os_, chunk, stage, sa, sb):
         with torch.cuda.device(dev):
             _lib.call("fss_dcf_eval_host", int(party), n, int(k.out_bits), count, ld,
                       _dev.ptr(seed0), _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(k.sigma_cw),
-                      _dev.ptr(k.leaf_cw), xh.data_ptr(), oh.data_ptr(), _dev.ptr(xs),
-                      _dev.ptr(os_), chunk, sa, sb)
+                      _dev.ptr(k.leaf_cw), xh, oh, _dev.ptr(xs), _dev.ptr(os_), chunk, stage,
+                      sa, sb)
     return _run_eval(launch, xt, host, count, dev, host_launch)
 
 

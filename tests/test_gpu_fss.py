@@ -357,3 +357,19 @@ def test_n64_tape_on_device_matches_numpy(oracle, pre):
     assert np.array_equal(_np(alpha), a) and np.array_equal(_np(k0.alpha_share), a0)
     assert np.array_equal(_np(k0.seed0), s0) and np.array_equal(_np(k1.seed0), s1)
     assert rng.bit_generator.state == ref.bit_generator.state
+
+
+def test_numpy_host_pipeline_matches_device_path():
+    # large numpy (pageable) inputs go through the staged native pipeline
+    N = (1 << 22) + 777
+    rng = np.random.default_rng(33)
+    alpha, k0, _ = fss.keygen_cmp(32, rng, N)
+    ea, e0, _ = fss.keygen_eq(32, rng, N)
+    x = np.random.default_rng(34).integers(0, 1 << 40, N, dtype=np.uint64)   # high bits ignored
+    xd = torch.from_numpy(x.view(np.int64)).cuda().view(torch.uint64)
+    y = fss.eval_cmp(0, k0, x)
+    assert isinstance(y, np.ndarray) and y.dtype == np.uint64
+    assert np.array_equal(y, _np(fss.eval_cmp(0, k0, xd)))
+    assert np.array_equal(fss.eval_eq(0, e0, x), _np(fss.eval_eq(0, e0, xd)))
+    yl, lv = fss.eval_cmp(0, k0, x, return_levels=True)
+    assert np.array_equal(yl, y) and lv.shape == (33, N)
