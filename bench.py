@@ -12,16 +12,21 @@ than the 126 MB L2, so no L2 flush is needed between steps). A step = eval_cmp
 for party 0 and party 1 over every element (two kernel launches).
 
 `e2e` = the same metric through the public drop-in API with host buffers: per
-step keygen_cmp(32, rng, N) from the host numpy Generator (tape drawn on device
-from its PCG64 state), eval_cmp for both parties on a pinned host x, shares
-copied back to pinned host memory. It includes keygen, so it is strictly more
-work per comparison than `value`.
+step eval_cmp for both parties on a pinned host x (keys dealt beforehand and
+resident in HBM, as in `value`), shares copied back to pinned host memory.
+`e2e.with_keygen` additionally runs keygen_cmp(32, rng, N) from the host numpy
+Generator (tape drawn on device from its PCG64 state) inside every step.
 
 `--impl reference` times the CPU restatement of the reference's algorithm
 (oracle/, C + AES-NI + OpenMP on all host cores; the Python reference itself
 cannot travel to the GPU box) on a bounded sample of the same workload.
-Multi-GPU (torchrun): every rank holds its own slice of keys for both parties
-(weak scaling, no data-path collective); time = max over ranks.
+Multi-GPU (torchrun): the N * 2^log2n keys are ONE global batch dealt by the
+sharded dealer (shard.keygen_cmp_shard: rank r draws only slice r of the shared
+PCG64 tape, bit-identical to a single-device keygen); every rank holds both
+parties' keys for its slice (weak scaling, no data-path collective in the timed
+step); time = max over ranks. Secondary (N >= 2): the output gather of both
+parties' shares to rank 0 (shard.gather_ring over NCCL) and the two-GPU sign
+protocol over NCCL and over peer memory.
 """
 
 from __future__ import annotations
@@ -308,12 +313,43 @@ def measure_pair_protocol(dev, xdev, rank, barrier, max_over_ranks, M=1 << 22, r
     return out
 
 
+def measure_gather(out0, out1, total, rank, barrier, max_over_ranks, reps=5):
+    """The output collective of SURVEY §8e: both parties' shares of every
+    rank's slice to rank 0 at the ring's wire width (shard.gather_ring: 4 B per
+    element per party at n = 32), then reconstructed there. Max over ranks of
+    the wall time per gather of both parties."""
+    import torch
+
+    from paper_2006_04593_b200 import shard
+
+    def once():
+        g0 = shard.gather_ring(out0, N_BITS, total, dst=0)
+        g1 = shard.gather_ring(out1, N_BITS, total, dst=0)
+        return g0, g1
+
+    g0, g1 = once()
+    if rank == 0:   # reconstruction of the gathered shares: one bit per comparison
+        rec = (g0.view(torch.int64) + g1.view(torch.int64)) & 0xFFFFFFFF
+        assert bool(((rec == 0) | (rec == 1)).all()), "gathered shares do not reconstruct to bits"
+    del g0, g1
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        once()
+    torch.cuda.synchronize()
+    t = max_over_ranks((time.perf_counter() - t0) / reps)
+    nbytes = 2 * total * 4
+    return {"elements": total, "ms_per_gather": t * 1e3, "bytes_to_rank0": nbytes,
+            "gb_per_s_into_rank0": nbytes / t / 1e9}
+
+
 def run_ours(args, ws, rank, local):
     import numpy as np
     import torch
     import torch.distributed as dist
 
-    from paper_2006_04593_b200 import _lib, fss
+    from paper_2006_04593_b200 import _lib, fss, shard
 
     _lib.load()  # fail loudly without the CUDA library
     # Test-only: FSS_BENCH_SAME_GPU=1 puts every rank on cuda:0 over gloo so the
@@ -345,8 +381,11 @@ def run_ours(args, ws, rank, local):
         return float(t.item())
 
     # ---- value: keys resident in HBM, device inputs ------------------------
-    rng = np.random.default_rng(1000 + rank)
-    alpha, k0, k1 = fss.keygen_cmp(N_BITS, rng, N, device=dev)
+    # rank r holds slice r of ONE global batch of N * ws keys (shard.py: the
+    # slice's tape is drawn at its offsets in the shared PCG64 stream, so the
+    # union over ranks is bit-identical to a single-device keygen of N * ws)
+    alpha, k0, k1 = shard.keygen_cmp_shard(N_BITS, np.random.default_rng(1000), N * ws, rank, ws,
+                                           device=dev)
     y = torch.randint(-(1 << 20), 1 << 20, (N,), device=dev, dtype=torch.int64)
     x = ((alpha.view(torch.int64) + y) & 0xFFFFFFFF).view(torch.uint64)
     out0 = out1 = None
@@ -403,6 +442,10 @@ def run_ours(args, ws, rank, local):
                                                              max_over_ranks)
         secondary["two_gpu_sign_protocol"] = measure_pair_protocol(dev, xdev, rank, barrier,
                                                                    max_over_ranks)
+    if ws >= 2 and not args.no_secondary:
+        secondary = dict(secondary or {})
+        secondary["output_gather"] = measure_gather(out0, out1, N * ws, rank, barrier,
+                                                    max_over_ranks)
     del out0, out1, rec
 
     # ---- e2e through the public API with host buffers ----------------------

@@ -73,6 +73,18 @@ int fss_pcg64_tape(const fss_pcg64_state* st, int n, uint64_t count, int draw_al
                    uint64_t* alpha, uint64_t* alpha0, uint8_t* s0, uint8_t* s1,
                    fss_pcg64_state* st_out, void* stream);
 
+/* Element slice [lo, lo + m) of the tape fss_pcg64_tape would draw for
+ * `count` elements, written from index 0 of each output (alpha, alpha0: m
+ * words; s0, s1: m x 16 bytes). Only the PCG64 outputs feeding the slice are
+ * generated (LCG jump-ahead), so one rank of a sharded dealer produces exactly
+ * its slice of the single-device tape. st_out describes the
+ * generator after the WHOLE count-element tape, so every rank advances its copy
+ * of the generator identically. New (no reference counterpart): the
+ * reference's dealer is single-process (dealer.py:96-103). */
+int fss_pcg64_tape_slice(const fss_pcg64_state* st, int n, uint64_t count, uint64_t lo, uint64_t m,
+                         int draw_alpha, uint64_t* alpha, uint64_t* alpha0, uint8_t* s0, uint8_t* s1,
+                         fss_pcg64_state* st_out, void* stream);
+
 /* The two random_seeds draws of _sample_tape alone (prg.py:36-40; s0 then s1)
  * -- the tail of the n = 64 tape, whose alpha / alpha0 are drawn by
  * fss_pcg64_ring_random (fss._uniform_ring's n == 64 branch, fss.py:48-50). */

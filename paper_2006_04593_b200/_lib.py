@@ -41,6 +41,8 @@ SIGNATURES = {
     "fss_mask_stream": [_u64, _u64, _u64, _u64, _int, _vp, _vp],
     "fss_pcg64_tape": [ctypes.POINTER(PcgState), _int, _u64, _int, _vp, _vp, _vp, _vp,
                        ctypes.POINTER(PcgState), _vp],
+    "fss_pcg64_tape_slice": [ctypes.POINTER(PcgState), _int, _u64, _u64, _u64, _int, _vp, _vp, _vp,
+                             _vp, ctypes.POINTER(PcgState), _vp],
     "fss_pcg64_seeds": [ctypes.POINTER(PcgState), _u64, _vp, _vp, ctypes.POINTER(PcgState), _vp],
     "fss_pcg64_ring_random": [ctypes.POINTER(PcgState), _int, _u64, _vp, ctypes.POINTER(PcgState), _vp],
     "fss_dpf_keygen": [_int, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],

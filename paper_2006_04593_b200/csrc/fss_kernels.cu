@@ -415,18 +415,26 @@ __device__ __forceinline__ uint64_t pcg_next(Pcg& p) {
 struct TapePlan {
     uint64_t state_lo, state_hi, inc_lo, inc_hi;
     int n;
-    uint64_t count;
+    uint64_t count;    // elements of the whole tape (numpy's `count`)
     int draw_alpha;    // alpha drawn (1) or given (0)
     int draw_alpha0;   // alpha0 drawn (1) or not (0: seeds-only tape)
     int has_uint32;    // numpy's buffered half-word present at start
     uint32_t uinteger;
     uint64_t raw64;    // number of 64-bit draws before the 32-bit stream (n > 32)
     uint64_t words;    // number of 32-bit words in the stream
+    // element slice [lo, hi) of the tape that is written (outputs indexed from
+    // lo), and the raw-output range [r_begin, r_end) one launch covers; the
+    // whole tape is lo = 0, hi = count, r = [0, total)
+    uint64_t lo, hi;
+    uint64_t r_begin, r_end;
+    int emit_buffered; // this launch writes word 0 (numpy's buffered half-word)
 };
 
-// Thread j handles raw outputs [j*kChunk, (j+1)*kChunk).
+// Thread j handles raw outputs [r_begin + j*kChunk, r_begin + (j+1)*kChunk).
 constexpr int kChunk = 16;
 
+// 32-bit word w of the stream -> its tape slot, written when its element lies
+// in the slice.
 __device__ __forceinline__ void emit_word(const TapePlan& P, uint64_t w, uint32_t v, uint64_t* alpha,
                                           uint64_t* alpha0, uint8_t* s0, uint8_t* s1) {
     const uint64_t N = P.count;
@@ -434,31 +442,31 @@ __device__ __forceinline__ void emit_word(const TapePlan& P, uint64_t w, uint32_
     if (P.n <= 32) {
         const int sh = 32 - P.n;
         if (P.draw_alpha) {
-            if (k < N) { alpha[k] = (uint64_t)(v >> sh); return; }
+            if (k < N) { if (k >= P.lo && k < P.hi) alpha[k - P.lo] = (uint64_t)(v >> sh); return; }
             k -= N;
         }
         if (P.draw_alpha0) {
-            if (k < N) { alpha0[k] = (uint64_t)(v >> sh); return; }
+            if (k < N) { if (k >= P.lo && k < P.hi) alpha0[k - P.lo] = (uint64_t)(v >> sh); return; }
             k -= N;
         }
     }
     // seeds: 4 words per seed, byte 15 top bit cleared (prg.random_seeds, prg.py:36-40)
     uint8_t* dst = k < 4 * N ? s0 : s1;
     if (k >= 4 * N) k -= 4 * N;
+    const uint64_t e = k >> 2;
+    if (e < P.lo || e >= P.hi) return;
     if ((k & 3) == 3) v &= 0x7FFFFFFFu;
-    reinterpret_cast<uint32_t*>(dst)[k] = v;
+    reinterpret_cast<uint32_t*>(dst)[k - 4 * P.lo] = v;
 }
 
 __global__ void pcg64_tape_kernel(TapePlan P, uint64_t* __restrict__ alpha, uint64_t* __restrict__ alpha0,
                                   uint8_t* __restrict__ s0, uint8_t* __restrict__ s1) {
     const uint64_t h = (uint64_t)P.has_uint32;
-    const uint64_t raw_words = (P.words - h + 1) / 2;     // 64-bit draws feeding the word stream
-    const uint64_t total = P.raw64 + raw_words;
     const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (j == 0 && h && P.words > 0) emit_word(P, 0, P.uinteger, alpha, alpha0, s0, s1);
-    const uint64_t begin = j * kChunk;
-    if (begin >= total) return;
-    const uint64_t end = begin + kChunk < total ? begin + kChunk : total;
+    if (j == 0 && P.emit_buffered) emit_word(P, 0, P.uinteger, alpha, alpha0, s0, s1);
+    const uint64_t begin = P.r_begin + j * kChunk;
+    if (begin >= P.r_end) return;
+    const uint64_t end = begin + kChunk < P.r_end ? begin + kChunk : P.r_end;
     Pcg p;
     p.state = ((unsigned __int128)P.state_hi << 64) | P.state_lo;
     p.inc = ((unsigned __int128)P.inc_hi << 64) | P.inc_lo;
@@ -470,10 +478,10 @@ __global__ void pcg64_tape_kernel(TapePlan P, uint64_t* __restrict__ alpha, uint
         if (r < P.raw64) {  // n > 32: 64-bit Lemire draws, v >> (64-n)
             uint64_t k = r;
             if (P.draw_alpha) {
-                if (k < N) { alpha[k] = v >> sh64; continue; }
+                if (k < N) { if (k >= P.lo && k < P.hi) alpha[k - P.lo] = v >> sh64; continue; }
                 k -= N;
             }
-            alpha0[k] = v >> sh64;
+            if (k >= P.lo && k < P.hi) alpha0[k - P.lo] = v >> sh64;
             continue;
         }
         const uint64_t q = r - P.raw64;
@@ -832,9 +840,31 @@ int fss_dcf_keygen(int n, int out_bits, uint64_t count, const uint64_t* alpha,
 
 namespace {
 
+// One launch over the raw outputs [r_begin, r_end) of plan P.
+int launch_tape_range(TapePlan P, uint64_t r_begin, uint64_t r_end, int emit_buffered, uint64_t* alpha,
+                      uint64_t* alpha0, uint8_t* s0, uint8_t* s1, void* stream) {
+    if (r_end <= r_begin && !emit_buffered) return kOk;
+    P.r_begin = r_begin;
+    P.r_end = r_end > r_begin ? r_end : r_begin;
+    P.emit_buffered = emit_buffered;
+    const uint64_t threads = (P.r_end - P.r_begin + kChunk - 1) / kChunk;
+    const int bs = 256;
+    const uint64_t grid = threads ? (threads + bs - 1) / bs : 1;
+    pcg64_tape_kernel<<<(unsigned)grid, bs, 0, (cudaStream_t)stream>>>(P, alpha, alpha0, s0, s1);
+    return check_launch();
+}
+
+// The tape of `count` elements (fss._sample_tape, fss.py:292-303), of which
+// only the element slice [lo, lo + m) is materialised (outputs indexed from 0).
+// A rank of a sharded dealer draws its slice of the global tape this way: the
+// raw PCG64 outputs feeding that slice are reached by LCG jump-ahead, so every
+// rank's keys equal the corresponding slice of a single-device keygen(count).
+// st_out always describes the state after the WHOLE tape.
 int launch_tape(const fss_pcg64_state* st, int n, uint64_t count, int draw_alpha, int draw_alpha0,
                 uint64_t* alpha, uint64_t* alpha0, uint8_t* s0, uint8_t* s1, fss_pcg64_state* st_out,
-                void* stream) {
+                void* stream, uint64_t lo = 0, uint64_t m = ~0ULL) {
+    if (m == ~0ULL) m = count - lo;
+    if (lo > count || m > count - lo) return set_err(kEinval, "tape slice out of range%s");
     TapePlan P;
     P.state_lo = st->state_lo; P.state_hi = st->state_hi;
     P.inc_lo = st->inc_lo; P.inc_hi = st->inc_hi;
@@ -842,6 +872,7 @@ int launch_tape(const fss_pcg64_state* st, int n, uint64_t count, int draw_alpha
     P.draw_alpha0 = draw_alpha0 ? 1 : 0;
     P.has_uint32 = st->has_uint32 ? 1 : 0;
     P.uinteger = st->uinteger;
+    P.lo = lo; P.hi = lo + m;
     const uint64_t na = (P.draw_alpha ? count : 0) + (P.draw_alpha0 ? count : 0);
     if (n <= 32) {
         P.raw64 = 0;
@@ -863,12 +894,33 @@ int launch_tape(const fss_pcg64_state* st, int n, uint64_t count, int draw_alpha
         st_out->has_uint32 = (P.words == 0) ? st->has_uint32 : (int)(fresh & 1);
         st_out->uinteger = 0;  // caller fills from the last raw output when has_uint32
     }
-    if (count == 0) return kOk;
-    const uint64_t threads = (total + kChunk - 1) / kChunk;
-    const int bs = 256;
-    const uint64_t grid = threads ? (threads + bs - 1) / bs : 1;
-    pcg64_tape_kernel<<<(unsigned)grid, bs, 0, (cudaStream_t)stream>>>(P, alpha, alpha0, s0, s1);
-    return check_launch();
+    if (m == 0) return kOk;
+    if (lo == 0 && m == count)  // the whole tape: one launch over every raw output
+        return launch_tape_range(P, 0, total, (int)(h && P.words > 0), alpha, alpha0, s0, s1, stream);
+    // a slice: one launch per tape segment, over the raws feeding [lo, lo + m)
+    auto words = [&](uint64_t a, uint64_t b) -> int {  // 32-bit words [a, b) of the stream
+        const uint64_t a1 = a > h ? a : h;
+        const int buffered = (int)(h && a == 0 && b > 0);
+        if (b <= a1) return launch_tape_range(P, 0, 0, buffered, alpha, alpha0, s0, s1, stream);
+        return launch_tape_range(P, P.raw64 + (a1 - h) / 2, P.raw64 + (b - 1 - h) / 2 + 1, buffered,
+                                 alpha, alpha0, s0, s1, stream);
+    };
+    uint64_t seg = 0;  // start of the current segment in its stream
+    if (n <= 32) {
+        if (P.draw_alpha) { if (int rc = words(seg + lo, seg + lo + m)) return rc; seg += count; }
+        if (P.draw_alpha0) { if (int rc = words(seg + lo, seg + lo + m)) return rc; seg += count; }
+    } else {
+        if (P.draw_alpha) {
+            if (int rc = launch_tape_range(P, lo, lo + m, 0, alpha, alpha0, s0, s1, stream)) return rc;
+            seg += count;
+        }
+        if (P.draw_alpha0)
+            if (int rc = launch_tape_range(P, seg + lo, seg + lo + m, 0, alpha, alpha0, s0, s1, stream))
+                return rc;
+        seg = 0;
+    }
+    if (int rc = words(seg + 4 * lo, seg + 4 * (lo + m))) return rc;
+    return words(seg + 4 * count + 4 * lo, seg + 4 * count + 4 * (lo + m));
 }
 
 }  // namespace
@@ -880,6 +932,13 @@ int fss_pcg64_tape(const fss_pcg64_state* st, int n, uint64_t count, int draw_al
                    fss_pcg64_state* st_out, void* stream) {
     if (n < 1 || n > 63) return set_err(kEinval, "device tape supports n <= 63%s");
     return launch_tape(st, n, count, draw_alpha, 1, alpha, alpha0, s0, s1, st_out, stream);
+}
+
+int fss_pcg64_tape_slice(const fss_pcg64_state* st, int n, uint64_t count, uint64_t lo, uint64_t m,
+                         int draw_alpha, uint64_t* alpha, uint64_t* alpha0, uint8_t* s0, uint8_t* s1,
+                         fss_pcg64_state* st_out, void* stream) {
+    if (n < 1 || n > 63) return set_err(kEinval, "device tape supports n <= 63%s");
+    return launch_tape(st, n, count, draw_alpha, 1, alpha, alpha0, s0, s1, st_out, stream, lo, m);
 }
 
 int fss_pcg64_seeds(const fss_pcg64_state* st, uint64_t count, uint8_t* s0, uint8_t* s1,
@@ -913,6 +972,7 @@ int fss_pcg64_ring_random(const fss_pcg64_state* st, int n_bits, uint64_t count,
     P.uinteger = st->uinteger;
     P.raw64 = count;
     P.words = count;
+    P.lo = 0; P.hi = count; P.r_begin = 0; P.r_end = 0; P.emit_buffered = 0;  // unused here
     const uint64_t h = (uint64_t)P.has_uint32;
     const uint64_t fresh = count > h ? count - h : 0;        // words drawn from new outputs
     if (st_out) {

@@ -246,9 +246,15 @@ def _device_tape_ok(n: int, rng) -> bool:
     return 1 <= n <= 63 and _pcg.is_pcg64(rng)
 
 
-def _sample_tape(n: int, rng, count: int, alpha, device):
+def _sample_tape(n: int, rng, count: int, alpha, device, shard=None):
     """fss._sample_tape (fss.py:292-303): draw order alpha (unless given),
-    alpha0, s0, s1 -- bit-identical to the reference's numpy draws."""
+    alpha0, s0, s1 -- bit-identical to the reference's numpy draws.
+
+    ``shard=(lo, m)`` materialises only the element slice [lo, lo + m) of the
+    ``count``-element tape (a given ``alpha`` is then the slice's, shape (m,));
+    ``rng`` still advances past the whole tape (see shard.py)."""
+    if shard is not None:
+        return _sample_tape_slice(n, rng, count, alpha, device, *shard)
     if alpha is not None:
         alpha_t = _dev.to_device_u64(alpha, device)
         if tuple(alpha_t.shape) != (count,):
@@ -286,6 +292,39 @@ def _sample_tape(n: int, rng, count: int, alpha, device):
                   _dev.ptr(a) if draw_alpha else None, _dev.ptr(a0), _dev.ptr(s0), _dev.ptr(s1),
                   out_st, _dev.stream_handle(device))
     _pcg.commit(rng, st, out_st, count > 0)   # advance the caller's rng exactly as numpy would
+    return a, a0, s0, s1
+
+
+def _sample_tape_slice(n: int, rng, count: int, alpha, device, lo: int, m: int):
+    if not (0 <= lo and 0 <= m and lo + m <= count):
+        raise ValueError(f"tape slice [{lo}, {lo + m}) outside a tape of {count}")
+    alpha_t = None
+    if alpha is not None:
+        alpha_t = _dev.to_device_u64(alpha, device)
+        if tuple(alpha_t.shape) != (m,):
+            raise ValueError("alpha must have shape (slice length,)")
+        from . import ring_ops
+        alpha_t = ring_ops.mask(alpha_t, n)
+    if not _device_tape_ok(n, rng):
+        # n = 64 (RingTensor.random two-call draw) or a non-PCG64 generator: draw
+        # the whole tape (on device / from the caller's generator) and keep the
+        # slice. Only the n <= 63 PCG64 path generates the slice alone.
+        full_alpha = None if alpha is None else torch.zeros(count, dtype=torch.uint64, device=device)
+        a, a0, s0, s1 = _sample_tape(n, rng, count, full_alpha, device)
+        a = alpha_t if alpha is not None else a[lo:lo + m].clone()
+        return a, a0[lo:lo + m].clone(), s0[lo:lo + m].clone(), s1[lo:lo + m].clone()
+    cst, st = _pcg.snapshot(rng)
+    out_st = PcgState()
+    draw_alpha = alpha is None
+    a = torch.empty(m, dtype=torch.uint64, device=device) if draw_alpha else alpha_t
+    a0 = torch.empty(m, dtype=torch.uint64, device=device)
+    s0 = torch.empty((m, 16), dtype=torch.uint8, device=device)
+    s1 = torch.empty((m, 16), dtype=torch.uint8, device=device)
+    with torch.cuda.device(device):
+        _lib.call("fss_pcg64_tape_slice", cst, n, count, lo, m, int(draw_alpha),
+                  _dev.ptr(a) if draw_alpha else None, _dev.ptr(a0), _dev.ptr(s0), _dev.ptr(s1),
+                  out_st, _dev.stream_handle(device))
+    _pcg.commit(rng, st, out_st, count > 0)   # the generator moves past the WHOLE tape
     return a, a0, s0, s1
 
 
@@ -350,12 +389,13 @@ def _keygen_cmp_core(n: int, alpha, alpha0, s0_init, s1_init, out_bits: int = No
 
 
 def keygen_eq(n: int, rng: np.random.Generator, count: int = 1,
-              alpha=None, device=None):
-    """Generate ``count`` equality key pairs; returns (alpha, k0, k1) (fss.py:306-313)."""
+              alpha=None, device=None, _shard=None):
+    """Generate ``count`` equality key pairs; returns (alpha, k0, k1) (fss.py:306-313).
+    ``_shard=(lo, m)``: only keys [lo, lo + m) of the batch (shard.keygen_eq_shard)."""
     if not 4 <= n <= 64:
         raise ValueError("equality keys support 4 <= n <= 64")
     dev = _dev.default_device(device)
-    a, a0, s0, s1 = _sample_tape(n, rng, count, alpha, dev)
+    a, a0, s0, s1 = _sample_tape(n, rng, count, alpha, dev, _shard)
     k0, k1 = _keygen_eq_core(n, a, a0, s0, s1)
     return a, k0, k1
 
@@ -366,14 +406,15 @@ def keygen_eq_with_tape(n: int, rng: np.random.Generator, count: int = 1, device
 
 
 def keygen_cmp(n: int, rng: np.random.Generator, count: int = 1,
-               alpha=None, out_bits: int = None, device=None):
-    """Generate ``count`` comparison key pairs; returns (alpha, k0, k1) (fss.py:321-335)."""
+               alpha=None, out_bits: int = None, device=None, _shard=None):
+    """Generate ``count`` comparison key pairs; returns (alpha, k0, k1) (fss.py:321-335).
+    ``_shard=(lo, m)``: only keys [lo, lo + m) of the batch (shard.keygen_cmp_shard)."""
     if not 4 <= n <= 63:
         raise ValueError("comparison keys support 4 <= n <= 63")
     if out_bits is not None and not n <= out_bits <= 63:
         raise ValueError("out_bits must lie in [n, 63]")
     dev = _dev.default_device(device)
-    a, a0, s0, s1 = _sample_tape(n, rng, count, alpha, dev)
+    a, a0, s0, s1 = _sample_tape(n, rng, count, alpha, dev, _shard)
     k0, k1 = _keygen_cmp_core(n, a, a0, s0, s1, out_bits)
     return a, k0, k1
 

@@ -1,0 +1,133 @@
+"""Element-sharded dealer and output gather across ranks.
+
+Every FSS element is independent, so a batch of ``total`` keys splits into
+contiguous slices, one per rank (one process per GPU); each rank holds BOTH
+parties' keys for its slice and runs keygen and evaluation with no data-path
+collective. This module supplies the two pieces around that:
+
+* ``keygen_cmp_shard`` / ``keygen_eq_shard``: rank r's slice of the keys that
+  ``fss.keygen_cmp(n, rng, total)`` would deal on one device -- bit-identical,
+  because the randomness tape of the slice is drawn straight from the caller's
+  numpy PCG64 stream at the slice's offsets (``fss_pcg64_tape_slice``, LCG
+  jump-ahead; no rank generates the other ranks' draws). Every rank passes a
+  generator in the same state and every rank's generator then advances past the
+  whole ``total``-element tape, exactly as the single-process dealer's would
+  (``Dealer._generate``, reference dealer.py:96-103), so successive sharded
+  calls stay in lock-step.
+* ``gather_shards`` / ``all_gather_shards`` / ``gather_ring``: the one output
+  collective of §8e -- the evaluated shares of every slice to rank ``dst`` (or to
+  all ranks) for reconstruction; ``gather_ring`` ships them at the ring's wire
+  width (4 B per element for n <= 32, the reference's ``pack_ring``,
+  sharing.py:191-207).
+
+The masked-message exchange between the two parties is the other collective and
+lives in ``runtime`` (``DistTransport`` over NCCL, ``PeerTransport`` over peer
+memory). Collectives use ``torch.distributed`` (NCCL for CUDA tensors on one
+process per GPU; gloo for host tensors in the CPU tests).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import fss
+
+
+def shard_bounds(total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced slice [lo, hi) of ``total`` elements owned by ``rank``
+    (sizes differ by at most one; ranks in order)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside a world of {world}")
+    if total < 0:
+        raise ValueError("total must be non-negative")
+    return total * rank // world, total * (rank + 1) // world
+
+
+def _rank_world(rank, world, group=None) -> tuple[int, int]:
+    if rank is None or world is None:
+        if not (dist.is_available() and dist.is_initialized()):
+            raise ValueError("pass rank and world, or initialise torch.distributed")
+        rank = dist.get_rank(group) if rank is None else rank
+        world = dist.get_world_size(group) if world is None else world
+    return int(rank), int(world)
+
+
+def keygen_cmp_shard(n: int, rng: np.random.Generator, total: int, rank: int = None,
+                     world: int = None, alpha=None, out_bits: int = None, device=None, group=None):
+    """Rank ``rank``'s slice of ``fss.keygen_cmp(n, rng, total, ...)``: returns
+    (alpha, k0, k1) for elements [lo, hi) = ``shard_bounds(total, rank, world)``.
+    A given ``alpha`` is the slice's (shape (hi - lo,))."""
+    rank, world = _rank_world(rank, world, group)
+    lo, hi = shard_bounds(total, rank, world)
+    return fss.keygen_cmp(n, rng, total, alpha=alpha, out_bits=out_bits, device=device,
+                          _shard=(lo, hi - lo))
+
+
+def keygen_eq_shard(n: int, rng: np.random.Generator, total: int, rank: int = None,
+                    world: int = None, alpha=None, device=None, group=None):
+    """Rank ``rank``'s slice of ``fss.keygen_eq(n, rng, total, ...)`` (see keygen_cmp_shard)."""
+    rank, world = _rank_world(rank, world, group)
+    lo, hi = shard_bounds(total, rank, world)
+    return fss.keygen_eq(n, rng, total, alpha=alpha, device=device, _shard=(lo, hi - lo))
+
+
+def _comm_device(t: torch.Tensor, group=None) -> torch.device:
+    # NCCL moves CUDA tensors (NVLink / NVSwitch); gloo moves host tensors
+    return t.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+
+
+def _collect(t: torch.Tensor, total: int, rank: int, world: int, dst, group):
+    lo, hi = shard_bounds(total, rank, world)
+    m = hi - lo
+    if t.shape[0] != m:
+        raise ValueError(f"rank {rank} holds {t.shape[0]} rows, its shard has {m}")
+    per = -(-total // world) if world else 0
+    tail = tuple(t.shape[1:])
+    row_elems = int(np.prod(tail)) if tail else 1
+    row_bytes = row_elems * t.element_size()
+    dev = _comm_device(t, group)
+    buf = torch.zeros((per, row_bytes), dtype=torch.uint8, device=dev)
+    if m:
+        buf[:m].copy_(t.contiguous().reshape(m, row_elems).view(torch.uint8))
+    if dst is None:
+        out = torch.empty((world * per, row_bytes), dtype=torch.uint8, device=dev)
+        dist.all_gather_into_tensor(out, buf, group=group)
+        parts = list(out.split(per))
+    else:
+        parts = [torch.empty_like(buf) for _ in range(world)] if rank == dst else None
+        dist.gather(buf, parts, dst=dst, group=group)
+        if rank != dst:
+            return None
+    rows = [parts[r][: shard_bounds(total, r, world)[1] - shard_bounds(total, r, world)[0]]
+            for r in range(world)]
+    flat = torch.cat(rows).to(t.device)
+    return flat.view(t.dtype).reshape((total,) + tail)
+
+
+def gather_shards(t: torch.Tensor, total: int, dst: int = 0, group=None):
+    """Concatenate every rank's slice (shape (hi - lo, ...), any dtype) on rank
+    ``dst``: returns the (total, ...) tensor there and None elsewhere."""
+    rank, world = _rank_world(None, None, group)
+    return _collect(t, total, rank, world, dst, group)
+
+
+def all_gather_shards(t: torch.Tensor, total: int, group=None):
+    """Every rank receives the concatenation of all slices, shape (total, ...)."""
+    rank, world = _rank_world(None, None, group)
+    return _collect(t, total, rank, world, None, group)
+
+
+def gather_ring(values: torch.Tensor, n_bits: int, total: int, dst=0, group=None):
+    """``gather_shards`` of ring values (u64, one per element) shipped at the
+    ring's wire width (sharing.pack_ring: 4 B per element for n <= 32); the
+    result is u64 again. ``dst=None`` gathers to every rank."""
+    from . import sharing
+    rank, world = _rank_world(None, None, group)
+    v = values.reshape(-1)
+    wire = sharing.pack_ring(v, n_bits) if v.is_cuda else v
+    got = _collect(wire, total, rank, world, dst, group)
+    if got is None:
+        return None
+    return sharing.unpack_ring(got, n_bits) if got.is_cuda else got

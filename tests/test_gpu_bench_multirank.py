@@ -1,5 +1,6 @@
 """bench.py's N>1 code path (torchrun, one process per rank, max-over-ranks
-timing, the NCCL masked-exchange secondary) exercised on a single-GPU box:
+timing, the sharded dealer, the NCCL masked-exchange and output-gather
+secondaries) exercised on a single-GPU box:
 FSS_BENCH_SAME_GPU=1 puts both ranks on cuda:0 over gloo. Only the contract
 is checked -- numbers from two ranks sharing one GPU are meaningless."""
 
@@ -41,3 +42,5 @@ def test_two_rank_bench_contract():
     pp = d["secondary"]["two_gpu_sign_protocol"]
     assert pp["nccl"]["comparisons_per_s_per_pair"] > 0
     assert pp["peer_memory"]["comparisons_per_s_per_pair"] > 0
+    g = d["secondary"]["output_gather"]   # both parties' shares of 2 x 2^18 elements to rank 0
+    assert g["elements"] == 2 << 18 and g["bytes_to_rank0"] == 2 * (2 << 18) * 4
