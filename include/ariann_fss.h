@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define FSS_ABI_VERSION 2
+#define FSS_ABI_VERSION 3
 #define FSS_OK 0
 #define FSS_EINVAL 1
 #define FSS_ECUDA 2
@@ -157,16 +157,17 @@ int fss_dpf_eval_host(int party, int n, uint64_t count, uint64_t ld, const uint8
 /* ARNK per-party payloads (LAYOUT.md:48-71; fss._pack_eq/_pack_cmp fss.py:540-583,
  * _unpack_eq/_unpack_cmp fss.py:553-602). kind 0 = equality, 1 = comparison.
  * payload is count * fss_arnk_elem_bytes(kind, n) bytes, element-major.
- * Pack reads level rows with stride ld; unpack writes ld = count.
+ * Level rows have stride ld >= count on both sides (ld > count addresses a
+ * column range of larger arrays, e.g. one chunk of a streamed key file).
  * Unused pointers (cw_final for cmp, sigma/leaf for eq) may be NULL. */
 uint64_t fss_arnk_elem_bytes(int kind, int n);
 int fss_arnk_pack(int kind, int n, uint64_t count, uint64_t ld, const uint64_t* alpha_share,
                   const uint8_t* seed0, const uint8_t* scw, const uint8_t* tcw,
                   const uint64_t* cw_final, const uint64_t* sigma_cw, const uint64_t* leaf_cw,
                   uint8_t* payload, void* stream);
-int fss_arnk_unpack(int kind, int n, uint64_t count, const uint8_t* payload, uint64_t* alpha_share,
-                    uint8_t* seed0, uint8_t* scw, uint8_t* tcw, uint64_t* cw_final,
-                    uint64_t* sigma_cw, uint64_t* leaf_cw, void* stream);
+int fss_arnk_unpack(int kind, int n, uint64_t count, uint64_t ld, const uint8_t* payload,
+                    uint64_t* alpha_share, uint8_t* seed0, uint8_t* scw, uint8_t* tcw,
+                    uint64_t* cw_final, uint64_t* sigma_cw, uint64_t* leaf_cw, void* stream);
 
 /* Elementwise ring arithmetic mod 2^n_bits (ring.py:99-129): out = op(a, b) & mask,
  * b == NULL uses b_scalar. NEG / MASK ignore b. out may alias a or b. */

@@ -33,6 +33,8 @@ class Peaks(ctypes.Structure):
 
 
 # name -> argtypes (all return int status unless listed in _RESTYPE)
+ABI_VERSION = 3   # include/ariann_fss.h FSS_ABI_VERSION
+
 SIGNATURES = {
     "fss_abi_version": [],
     "fss_last_error": [],
@@ -55,7 +57,7 @@ SIGNATURES = {
     "fss_dpf_eval_host": [_int, _int, _u64, _u64] + [_vp] * 8 + [_u64, _vp, _vp, _vp],
     "fss_arnk_elem_bytes": [_int, _int],
     "fss_arnk_pack": [_int, _int, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
-    "fss_arnk_unpack": [_int, _int, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "fss_arnk_unpack": [_int, _int, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "fss_ring_op": [_int, _int, _u64, _vp, _vp, _u64, _vp, _vp],
     "fss_beaver_mul": [_int, _int, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "fss_wire_bytes": [_int],
@@ -88,6 +90,9 @@ def load():
             fn = getattr(lib, name)
             fn.argtypes = argtypes
             fn.restype = _RESTYPE.get(name, ctypes.c_int)
+        if lib.fss_abi_version() != ABI_VERSION:
+            raise ImportError(f"{LIB} has ABI {lib.fss_abi_version()}, this package needs "
+                              f"{ABI_VERSION}: rebuild it (__graft_entry__.build())")
         _lib = lib
     return _lib
 

@@ -4,9 +4,15 @@
 // Element layout (w = ceil(n/8) little-endian bytes per ring value):
 //   eq : alpha_share[w] | seed0[16] | n x (scw[16] | flags[1])           | cw_final[w]
 //   cmp: alpha_share[w] | seed0[16] | n x (scw[16] | flags[1] | sigma[w]) | (n+1) x leaf[w]
-// Grid: x over elements, y over "slots" (slot i < n = level i's record,
-// slot n = head + eq tail, slot n+1 = cmp leaf block). Each thread moves one
-// slot of one element.
+//
+// Tiled transpose through shared memory. A CTA owns a tile of E consecutive
+// elements: their payload records are one contiguous byte range of HBM
+// (E * elem bytes), moved between HBM and shared memory with 16-byte vector
+// accesses; the level-major key rows of the tile (scw[i][e0 .. e0+E), tcw,
+// sigma, leaf, ...) are read / written with consecutive threads on consecutive
+// elements, i.e. coalesced. All byte-level (re)assembly happens in shared
+// memory, so HBM traffic is the algorithmic bytes: the payload once plus the
+// key arrays once.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -14,17 +20,11 @@
 #include "../../include/ariann_fss.h"
 #include "common.cuh"
 
+#ifndef FSSB_ARNK_NAIVE
+#define FSSB_ARNK_NAIVE 0
+#endif
+
 namespace {
-
-__device__ __forceinline__ void put_le(uint8_t* p, uint64_t v, int w) {
-    for (int b = 0; b < w; b++) p[b] = (uint8_t)(v >> (8 * b));
-}
-
-__device__ __forceinline__ uint64_t get_le(const uint8_t* p, int w) {
-    uint64_t v = 0;
-    for (int b = 0; b < w; b++) v |= (uint64_t)p[b] << (8 * b);
-    return v;
-}
 
 __host__ __device__ __forceinline__ uint64_t elem_bytes(int kind, int n) {
     const int w = (n + 7) / 8;
@@ -41,6 +41,21 @@ struct Keys {
     uint64_t* leaf_cw;   // cmp
 };
 
+#if FSSB_ARNK_NAIVE
+__device__ __forceinline__ void put_le(uint8_t* p, uint64_t v, int w) {
+    for (int b = 0; b < w; b++) p[b] = (uint8_t)(v >> (8 * b));
+}
+
+__device__ __forceinline__ uint64_t get_le(const uint8_t* p, int w) {
+    uint64_t v = 0;
+    for (int b = 0; b < w; b++) v |= (uint64_t)p[b] << (8 * b);
+    return v;
+}
+
+// Round-1 first cut, kept for the variant sweep (scripts/aes_variants.py):
+// one thread per (element, slot), byte loads / stores straight to the
+// element-major payload in HBM -- a warp's 32 lanes touch 32 different lines
+// per byte instruction.
 template <bool PACK>
 __global__ void arnk_kernel(int kind, int n, uint64_t count, uint64_t ld, Keys k, uint8_t* buf) {
     const uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -87,18 +102,399 @@ __global__ void arnk_kernel(int kind, int n, uint64_t count, uint64_t ld, Keys k
         }
     }
 }
+#endif
+
+constexpr int kArnkThreads = 256;
+
+__device__ __forceinline__ uint32_t sld32(const uint8_t* s, uint32_t off) {
+    return *reinterpret_cast<const uint32_t*>(s + off);
+}
+
+// NB (<= 8) little-endian bytes at any byte offset of the shared tile (the
+// tile buffer has 16 bytes of slack so the covering word reads stay in bounds).
+template <int NB>
+__device__ __forceinline__ uint64_t sget(const uint8_t* s, uint32_t off) {
+    const uint32_t a = off & ~3u, sh = (off & 3u) * 8u;
+    const uint32_t w0 = sld32(s, a), w1 = sld32(s, a + 4);
+    uint64_t v = __funnelshift_r(w0, w1, sh);
+    if (NB > 4) v |= (uint64_t)__funnelshift_r(w1, sld32(s, a + 8), sh) << 32;
+    return NB >= 8 ? v : v & ((1ULL << (8 * NB)) - 1);
+}
+
+__device__ __forceinline__ uint4 sget16(const uint8_t* s, uint32_t off) {
+    const uint32_t a = off & ~3u, sh = (off & 3u) * 8u;
+    const uint32_t w0 = sld32(s, a), w1 = sld32(s, a + 4), w2 = sld32(s, a + 8), w3 = sld32(s, a + 12),
+                   w4 = sld32(s, a + 16);
+    return make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
+                      __funnelshift_r(w3, w4, sh));
+}
+
+// Store the NB (<= 28) bytes of the little-endian byte stream R[0..6] at tile
+// offset A + r (A word-aligned, r = offset mod 4, both layouts compile-time
+// after unrolling): whole aligned words as 32-bit stores, only the partial
+// words at either end byte by byte (their other bytes belong to neighbouring
+// fields written by other threads). Aligned word k holds stream bytes
+// [4k - r, 4k - r + 4).
+template <int r, int NB>
+__device__ __forceinline__ void sput_stream_r(uint8_t* s, uint32_t A, const uint32_t (&R)[7]) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const int lo = 4 * k - r;
+        if (lo >= NB) break;
+        const uint32_t prev = k > 0 ? R[k - 1] : 0u;
+        const uint32_t cur = k < 7 ? R[k] : 0u;
+        const uint32_t v = r ? __funnelshift_l(prev, cur, 8 * r) : cur;
+        if (lo >= 0 && lo + 4 <= NB) {
+            *reinterpret_cast<uint32_t*>(s + A + 4 * k) = v;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+                if (lo + j >= 0 && lo + j < NB) s[A + 4 * k + j] = (uint8_t)(v >> (8 * j));
+        }
+    }
+}
+
+template <int NB>
+__device__ __forceinline__ void sput_stream(uint8_t* s, uint32_t o, const uint32_t (&R)[7]) {
+    const uint32_t A = o & ~3u;
+    switch (o & 3u) {   // uniform across a warp whenever the record stride is word-aligned
+        case 0: sput_stream_r<0, NB>(s, A, R); break;
+        case 1: sput_stream_r<1, NB>(s, A, R); break;
+        case 2: sput_stream_r<2, NB>(s, A, R); break;
+        default: sput_stream_r<3, NB>(s, A, R); break;
+    }
+}
+
+template <int NB>
+__device__ __forceinline__ void sput_u64(uint8_t* s, uint32_t o, uint64_t v) {
+    const uint32_t R[7] = {(uint32_t)v, (uint32_t)(v >> 32), 0, 0, 0, 0, 0};
+    sput_stream<NB>(s, o, R);
+}
+
+__device__ __forceinline__ void sput16(uint8_t* s, uint32_t o, uint4 v) {
+    const uint32_t R[7] = {v.x, v.y, v.z, v.w, 0, 0, 0};
+    sput_stream<16>(s, o, R);
+}
+
+// Cooperative byte-range copy with the widest access both ends allow.
+__device__ __forceinline__ void copy_range(uint8_t* dst, const uint8_t* src, uint64_t nbytes) {
+    const uintptr_t mis = ((uintptr_t)dst | (uintptr_t)src);
+    if ((mis & 15) == 0) {
+        const uint64_t n16 = nbytes / 16;
+        for (uint64_t i = threadIdx.x; i < n16; i += blockDim.x)
+            reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+        for (uint64_t i = 16 * n16 + threadIdx.x; i < nbytes; i += blockDim.x) dst[i] = src[i];
+    } else if ((mis & 3) == 0) {
+        const uint64_t n4 = nbytes / 4;
+        for (uint64_t i = threadIdx.x; i < n4; i += blockDim.x)
+            reinterpret_cast<uint32_t*>(dst)[i] = reinterpret_cast<const uint32_t*>(src)[i];
+        for (uint64_t i = 4 * n4 + threadIdx.x; i < nbytes; i += blockDim.x) dst[i] = src[i];
+    } else {
+        for (uint64_t i = threadIdx.x; i < nbytes; i += blockDim.x) dst[i] = src[i];
+    }
+}
+
+// Work-item mapping for `rows` level-major rows x the E elements of a tile
+// (E = 16 << lnb): each half-warp takes 16 consecutive elements of one row and
+// the two half-warps of a warp take rows r and r + d (d = 1 << ld_). Row
+// accesses in HBM stay coalesced (16 consecutive elements). In shared memory
+// the 16 elements of one row, EB bytes apart, spread over 16 banks, and d is
+// chosen so that d * rowbytes = 4 (mod 8) -- an odd number of words: the
+// second row lands on the other 16 banks at the same byte alignment, so all
+// 32 lanes take the same store path. Shifts only, no divisions.
+__host__ __device__ __forceinline__ int row_step_log2(uint32_t rowbytes) {
+    for (int l = 0; l <= 2; l++)
+        if (((rowbytes << l) & 7u) == 4u) return l;
+    return 0;
+}
+
+struct Item {
+    uint32_t row, e;
+};
+
+__device__ __forceinline__ uint32_t pair_items(uint32_t rows, int lnb, int ld_) {
+    const uint32_t blocks = (rows + (2u << ld_) - 1) >> (ld_ + 1);
+    return (blocks << (ld_ + lnb)) * 32u;
+}
+
+__device__ __forceinline__ Item pair_item(uint32_t idx, int lnb, int ld_) {
+    const uint32_t q = idx >> 5;
+    const uint32_t pr = q >> lnb, eb = q & ((1u << lnb) - 1);
+    const uint32_t blk = pr >> ld_, r0 = pr & ((1u << ld_) - 1);
+    Item it;
+    it.row = (blk << (ld_ + 1)) + r0 + (((idx >> 4) & 1u) << ld_);
+    it.e = (eb << 4) + (idx & 15u);
+    return it;
+}
+
+// ---- bulk asynchronous copies (TMA engine, cp.async.bulk) -------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+#ifndef FSSB_ARNK_BATCH
+#define FSSB_ARNK_BATCH 4
+#endif
+constexpr int kBatch = FSSB_ARNK_BATCH;   // row loads in flight per thread (pack)
+
+// Tiles are double-buffered per CTA: while the threads transpose tile j in one
+// buffer, the TMA engine moves tile j+1 in (unpack) or tile j-1 out (pack) of
+// the other, so the payload side of the transfer costs no thread time. A tile
+// whose byte range is not 16-byte aligned (only the last, partial tile can be)
+// falls back to a cooperative copy. KIND and the ring width W are template
+// parameters so every record layout is compile-time.
+template <bool PACK, int KIND, int W>
+__global__ void __launch_bounds__(kArnkThreads)
+arnk_tile_kernel(int n, uint64_t count, uint64_t ld, int lnb, uint32_t stride, Keys k, uint8_t* buf) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    constexpr uint32_t rec = KIND == 0 ? 17 : 17 + W;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);       // 2 mbarriers
+    uint8_t* tiles_base = smem + 128;
+    const uint32_t E = 16u << lnb;
+    const uint32_t EB = (uint32_t)elem_bytes(KIND, n);
+    const uint32_t tail = W + 16 + n * rec;   // cw_final (eq) / leaf block (cmp)
+    const int d_lv = row_step_log2(rec), d_leaf = row_step_log2(W);
+    const uint64_t tiles = (count + E - 1) / E;
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0]);
+        mbar_init(&bars[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t parity = 0;   // bit b: phase of buffer b's mbarrier
+
+    auto tile_m = [&](uint64_t t) { return (uint32_t)(count - t * E < (uint64_t)E ? count - t * E : E); };
+    auto aligned = [&](uint32_t bytes, const uint8_t* gp) {
+        return (bytes & 15u) == 0 && ((uintptr_t)gp & 15u) == 0;
+    };
+    // unpack: bring tile t into buffer b (async when aligned)
+    auto fetch = [&](uint64_t t, int b) {
+        const uint32_t bytes = tile_m(t) * EB;
+        const uint8_t* gp = buf + t * E * EB;
+        uint8_t* dst = tiles_base + b * stride;
+        if (aligned(bytes, gp)) {
+            if (threadIdx.x == 0) bulk_load(dst, gp, bytes, &bars[b]);
+        } else {
+            copy_range(dst, gp, bytes);
+        }
+    };
+
+    int j = 0;
+    if (!PACK && blockIdx.x < tiles) fetch(blockIdx.x, 0);
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, j++) {
+        const int cur = j & 1;
+        uint8_t* tile = tiles_base + cur * stride;
+        const uint32_t m = tile_m(t);
+        const uint64_t e0 = t * E;
+        uint8_t* gp = buf + e0 * EB;
+        const bool async_io = aligned(m * EB, gp);
+        if (!PACK) {
+            const uint64_t tn = t + gridDim.x;
+            if (tn < tiles) fetch(tn, cur ^ 1);    // buffer cur^1 was released at the end of j-1
+            if (async_io) {
+                mbar_wait(&bars[cur], (parity >> cur) & 1u);
+                parity ^= 1u << cur;
+            } else {
+                __syncthreads();
+            }
+        } else {
+            // the bulk store issued from this buffer two tiles ago must have
+            // finished reading it (only the newest group may still be in flight)
+            if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncthreads();
+        }
+        // per-level records (scw | flags | sigma)
+        const uint32_t items = pair_items((uint32_t)n, lnb, d_lv);
+        if (PACK) {
+            for (uint32_t base = threadIdx.x; base < items; base += kBatch * kArnkThreads) {
+                uint4 v[kBatch];
+                uint32_t f[kBatch], so[kBatch];
+                uint64_t sg[kBatch];
+                bool ok[kBatch];
+#pragma unroll
+                for (int u = 0; u < kBatch; u++) {   // all loads first: kBatch rows in flight
+                    const uint32_t idx = base + u * kArnkThreads;
+                    const Item it = pair_item(idx, lnb, d_lv);
+                    ok[u] = idx < items && it.row < (uint32_t)n && it.e < m;
+                    if (ok[u]) {
+                        const uint64_t off = (uint64_t)it.row * ld + e0 + it.e;
+                        v[u] = *reinterpret_cast<const uint4*>(k.scw + 16 * off);
+                        f[u] = k.tcw[off];
+                        sg[u] = KIND == 1 ? k.sigma_cw[off] : 0;
+                        so[u] = it.e * EB + W + 16 + it.row * rec;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kBatch; u++) {
+                    if (!ok[u]) continue;
+                    const uint32_t R[7] = {v[u].x, v[u].y, v[u].z, v[u].w, f[u] | ((uint32_t)sg[u] << 8),
+                                           (uint32_t)(sg[u] >> 24), (uint32_t)(sg[u] >> 56)};
+                    sput_stream<rec>(tile, so[u], R);
+                }
+            }
+        } else {
+            for (uint32_t idx = threadIdx.x; idx < items; idx += kArnkThreads) {
+                const Item it = pair_item(idx, lnb, d_lv);
+                if (it.row >= (uint32_t)n || it.e >= m) continue;
+                const uint64_t off = (uint64_t)it.row * ld + e0 + it.e;
+                const uint32_t so = it.e * EB + W + 16 + it.row * rec;
+                *reinterpret_cast<uint4*>(k.scw + 16 * off) = sget16(tile, so);
+                k.tcw[off] = tile[so + 16];
+                if (KIND == 1) k.sigma_cw[off] = sget<W>(tile, so + 17);
+            }
+        }
+        // element head (alpha share, seed) and the eq tail (cw_final)
+        for (uint32_t e = threadIdx.x; e < m; e += kArnkThreads) {
+            const uint32_t so = e * EB;
+            if (PACK) {
+                sput_u64<W>(tile, so, k.alpha_share[e0 + e]);
+                sput16(tile, so + W, *reinterpret_cast<const uint4*>(k.seed0 + 16 * (e0 + e)));
+                if (KIND == 0) sput_u64<W>(tile, so + tail, k.cw_final[e0 + e]);
+            } else {
+                k.alpha_share[e0 + e] = sget<W>(tile, so);
+                *reinterpret_cast<uint4*>(k.seed0 + 16 * (e0 + e)) = sget16(tile, so + W);
+                if (KIND == 0) k.cw_final[e0 + e] = sget<W>(tile, so + tail);
+            }
+        }
+        // cmp leaf block: n + 1 rows of W-byte values
+        if (KIND == 1) {
+            const uint32_t leaf_items = pair_items((uint32_t)n + 1, lnb, d_leaf);
+            if (PACK) {
+                for (uint32_t base = threadIdx.x; base < leaf_items; base += kBatch * kArnkThreads) {
+                    uint64_t v[kBatch];
+                    uint32_t so[kBatch];
+                    bool ok[kBatch];
+#pragma unroll
+                    for (int u = 0; u < kBatch; u++) {
+                        const uint32_t idx = base + u * kArnkThreads;
+                        const Item it = pair_item(idx, lnb, d_leaf);
+                        ok[u] = idx < leaf_items && it.row <= (uint32_t)n && it.e < m;
+                        if (ok[u]) {
+                            v[u] = k.leaf_cw[(uint64_t)it.row * ld + e0 + it.e];
+                            so[u] = it.e * EB + tail + it.row * W;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kBatch; u++)
+                        if (ok[u]) sput_u64<W>(tile, so[u], v[u]);
+                }
+            } else {
+                for (uint32_t idx = threadIdx.x; idx < leaf_items; idx += kArnkThreads) {
+                    const Item it = pair_item(idx, lnb, d_leaf);
+                    if (it.row > (uint32_t)n || it.e >= m) continue;
+                    k.leaf_cw[(uint64_t)it.row * ld + e0 + it.e] = sget<W>(tile, it.e * EB + tail + it.row * W);
+                }
+            }
+        }
+        if (PACK) {
+            // generic-proxy smem writes -> visible to the TMA (async proxy) read
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (async_io) {
+                if (threadIdx.x == 0) bulk_store(gp, tile, m * EB);
+            } else {
+                copy_range(gp, tile, (uint64_t)m * EB);
+                if (threadIdx.x == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+        } else {
+            __syncthreads();   // tile consumed: its buffer may be refilled
+        }
+    }
+    if (PACK && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// Tile of E = 16 << lnb elements: 64 when two tile buffers fit 100 KiB of
+// shared memory, else 32 (largest record: cmp n = 63, 2,111 B).
+#ifndef FSSB_ARNK_TILE_KB
+#define FSSB_ARNK_TILE_KB 100
+#endif
+int arnk_tile_lnb(int kind, int n) { return 2 * elem_bytes(kind, n) * 64 <= FSSB_ARNK_TILE_KB * 1024 ? 2 : 1; }
+
+template <bool PACK, int KIND, int W>
+cudaError_t launch_tile(int n, uint64_t count, uint64_t ld, Keys k, uint8_t* buf, cudaStream_t st) {
+    const int lnb = arnk_tile_lnb(KIND, n);
+    const uint32_t E = 16u << lnb;
+    // per buffer: the tile + 16 bytes of slack for the covering word reads,
+    // rounded to 128 bytes; plus 128 bytes for the two mbarriers
+    const uint32_t stride = (uint32_t)((elem_bytes(KIND, n) * E + 16 + 127) / 128 * 128);
+    const size_t smem = 128 + 2 * (size_t)stride;
+    int dev = 0, sms = 0, per_sm = 1;
+    auto kern = arnk_tile_kernel<PACK, KIND, W>;
+    cudaError_t err = cudaGetDevice(&dev);
+    if (err == cudaSuccess) err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (err == cudaSuccess) err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err == cudaSuccess) err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kArnkThreads, smem);
+    if (err != cudaSuccess) return err;
+    const uint64_t tiles = (count + E - 1) / E;
+    const uint64_t cap = (uint64_t)sms * (per_sm > 0 ? per_sm : 1);
+    kern<<<(unsigned)(tiles < cap ? tiles : cap), kArnkThreads, smem, st>>>(n, count, ld, lnb, stride, k, buf);
+    return cudaGetLastError();
+}
+
+template <bool PACK, int KIND>
+cudaError_t launch_kind(int n, uint64_t count, uint64_t ld, Keys k, uint8_t* buf, cudaStream_t st) {
+    switch ((n + 7) / 8) {
+        case 1: return launch_tile<PACK, KIND, 1>(n, count, ld, k, buf, st);
+        case 2: return launch_tile<PACK, KIND, 2>(n, count, ld, k, buf, st);
+        case 3: return launch_tile<PACK, KIND, 3>(n, count, ld, k, buf, st);
+        case 4: return launch_tile<PACK, KIND, 4>(n, count, ld, k, buf, st);
+        case 5: return launch_tile<PACK, KIND, 5>(n, count, ld, k, buf, st);
+        case 6: return launch_tile<PACK, KIND, 6>(n, count, ld, k, buf, st);
+        case 7: return launch_tile<PACK, KIND, 7>(n, count, ld, k, buf, st);
+        default: return launch_tile<PACK, KIND, 8>(n, count, ld, k, buf, st);
+    }
+}
 
 int launch(bool pack, int kind, int n, uint64_t count, uint64_t ld, Keys k, uint8_t* buf, void* stream) {
     if ((kind != 0 && kind != 1) || n < 1 || n > 64 || (kind == 1 && n > 63))
         return fssb::set_error(FSS_EINVAL, "ARNK: bad kind or n");
+    if (ld < count) return fssb::set_error(FSS_EINVAL, "ARNK: level stride ld < count");
     if (count == 0) return FSS_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+#if FSSB_ARNK_NAIVE
     const int bs = 256;
     dim3 grid((unsigned)((count + bs - 1) / bs), kind == 0 ? n + 1 : n + 2);
     if (pack)
-        arnk_kernel<true><<<grid, bs, 0, (cudaStream_t)stream>>>(kind, n, count, ld, k, buf);
+        arnk_kernel<true><<<grid, bs, 0, st>>>(kind, n, count, ld, k, buf);
     else
-        arnk_kernel<false><<<grid, bs, 0, (cudaStream_t)stream>>>(kind, n, count, ld, k, buf);
+        arnk_kernel<false><<<grid, bs, 0, st>>>(kind, n, count, ld, k, buf);
     const cudaError_t err = cudaGetLastError();
+#else
+    const cudaError_t err = pack ? (kind ? launch_kind<true, 1>(n, count, ld, k, buf, st)
+                                         : launch_kind<true, 0>(n, count, ld, k, buf, st))
+                                 : (kind ? launch_kind<false, 1>(n, count, ld, k, buf, st)
+                                         : launch_kind<false, 0>(n, count, ld, k, buf, st));
+#endif
     return err == cudaSuccess ? FSS_OK : fssb::set_error(FSS_ECUDA, cudaGetErrorString(err));
 }
 
@@ -118,11 +514,11 @@ int fss_arnk_pack(int kind, int n, uint64_t count, uint64_t ld, const uint64_t* 
     return launch(true, kind, n, count, ld, k, payload, stream);
 }
 
-int fss_arnk_unpack(int kind, int n, uint64_t count, const uint8_t* payload, uint64_t* alpha_share,
-                    uint8_t* seed0, uint8_t* scw, uint8_t* tcw, uint64_t* cw_final,
-                    uint64_t* sigma_cw, uint64_t* leaf_cw, void* stream) {
+int fss_arnk_unpack(int kind, int n, uint64_t count, uint64_t ld, const uint8_t* payload,
+                    uint64_t* alpha_share, uint8_t* seed0, uint8_t* scw, uint8_t* tcw,
+                    uint64_t* cw_final, uint64_t* sigma_cw, uint64_t* leaf_cw, void* stream) {
     Keys k{alpha_share, seed0, scw, tcw, cw_final, sigma_cw, leaf_cw};
-    return launch(false, kind, n, count, count, k, const_cast<uint8_t*>(payload), stream);
+    return launch(false, kind, n, count, ld, k, const_cast<uint8_t*>(payload), stream);
 }
 
 }  // extern "C"

@@ -791,7 +791,7 @@ def _unpack(kind: int, party: int, n: int, count: int, payload, device=None):
         sigma = torch.empty((n, count), dtype=torch.uint64, device=dev)
         leaf = torch.empty((n + 1, count), dtype=torch.uint64, device=dev)
     with torch.cuda.device(dev):
-        _lib.call("fss_arnk_unpack", kind, n, count, _dev.ptr(buf), _dev.ptr(alpha),
+        _lib.call("fss_arnk_unpack", kind, n, count, count, _dev.ptr(buf), _dev.ptr(alpha),
                   _dev.ptr(seed0), _dev.ptr(scw), _dev.ptr(tcw), _dev.ptr(cw_final),
                   _dev.ptr(sigma), _dev.ptr(leaf), _dev.stream_handle(dev))
     if kind == KIND_EQ:
