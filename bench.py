@@ -249,6 +249,23 @@ def measure_secondary(dev, args):
     rec = (fss.eval_eq(0, e0, x).view(torch.int64) + fss.eval_eq(1, e1, x).view(torch.int64)) & 0xFFFFFFFF
     assert bool((rec == 1).all()), "DPF reconstruction mismatch"
     del alpha, e0, e1, x, rec
+    # ARNK key (de)serialisation of one party's DCF keys (fss_arnk_pack /
+    # fss_arnk_unpack): HBM-bound byte transposes; algorithmic bytes per key =
+    # the 824-B payload + the 1,088 B of key arrays, each moved once
+    _, c0, _ = fss.keygen_cmp(N_BITS, rng, N, device=dev)
+    payload = fss._pack_device(c0).reshape(-1)
+    per_key = fss.cmp_elem_bytes(N_BITS) + 8 + 16 + 16 * N_BITS + N_BITS + 8 * N_BITS + 8 * (N_BITS + 1)
+    t = timed(lambda: fss._pack_device(c0))
+    out["arnk_pack_keys_per_s"] = N / t
+    out["arnk_pack_gb_per_s"] = N * per_key / t / 1e9
+    t = timed(lambda: fss._unpack(fss.KIND_CMP, 0, N_BITS, N, payload, dev))
+    out["arnk_unpack_keys_per_s"] = N / t
+    out["arnk_unpack_gb_per_s"] = N * per_key / t / 1e9
+    out["arnk_algorithmic_bytes_per_key"] = per_key
+    back = fss._unpack(fss.KIND_CMP, 0, N_BITS, N, payload, dev)
+    assert torch.equal(back.scw, c0.scw) and torch.equal(back.leaf_cw.view(torch.int64),
+                                                         c0.leaf_cw.view(torch.int64)), "ARNK round trip"
+    del c0, payload, back
     torch.cuda.empty_cache()
     return out
 
@@ -426,6 +443,8 @@ def run_ours(args, ws, rank, local):
     except (OSError, ValueError):
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = ("MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks
+               else "fallback 6.65 TB/s of B200_PROFILING.md (MEASURED_PEAKS.json absent on this box)")
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     traffic = load_traffic()
     props = torch.cuda.get_device_properties(dev)
@@ -436,6 +455,9 @@ def run_ours(args, ws, rank, local):
     lds_peak_lookups = peaks_live["lds_wavefronts_per_s"] * 32
     alu_peak_aes = peaks_live["lop3_lane_ops_per_s"] / LOP3_PER_AES_BITSLICED
     secondary = measure_secondary(dev, args) if not args.no_secondary else None
+    if secondary:
+        for op in ("pack", "unpack"):
+            secondary[f"arnk_{op}_frac_hbm"] = secondary[f"arnk_{op}_gb_per_s"] / hbm_peak
     if ws >= 2 and ws % 2 == 0 and not args.no_secondary:
         secondary = dict(secondary or {})
         secondary["nccl_masked_exchange"] = measure_exchange(dev, xdev, rank, ws, N, barrier,
@@ -544,8 +566,7 @@ def run_ours(args, ws, rank, local):
                                   f"{LOP3_PER_AES_BITSLICED} LOP3 per block")},
         "hbm_roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved_gbs / hbm_peak,
-                         "note": f"{BYTES_PER_EVAL} algorithmic B per party-eval; peak = "
-                                 "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+                         "note": f"{BYTES_PER_EVAL} algorithmic B per party-eval; peak = {hbm_src}"},
         "peaks_probe": peaks_live,
         "secondary": secondary,
         "kernel_ms_per_launch": avg_launch_s * 1e3,

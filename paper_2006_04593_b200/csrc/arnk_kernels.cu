@@ -433,16 +433,25 @@ arnk_tile_kernel(int n, uint64_t count, uint64_t ld, int lnb, uint32_t stride, K
     if (PACK && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-// Tile of E = 16 << lnb elements: 64 when two tile buffers fit 100 KiB of
-// shared memory, else 32 (largest record: cmp n = 63, 2,111 B).
+// Tile of E = 16 << lnb elements, two tile buffers per CTA. Unpack: 64
+// elements whenever the two buffers fit 110 KiB (cmp n = 32: 2 x 52.7 KB, two
+// CTAs per SM); pack: 64 only up to 100 KiB, i.e. 32 for cmp n = 32 (four
+// CTAs per SM hide its row-load latency better) -- measured,
+// profiles/r01_arnk_variants.json. Largest record: cmp n = 63, 2,111 B.
 #ifndef FSSB_ARNK_TILE_KB
 #define FSSB_ARNK_TILE_KB 100
 #endif
-int arnk_tile_lnb(int kind, int n) { return 2 * elem_bytes(kind, n) * 64 <= FSSB_ARNK_TILE_KB * 1024 ? 2 : 1; }
+#ifndef FSSB_ARNK_UNPACK_TILE_KB
+#define FSSB_ARNK_UNPACK_TILE_KB 110
+#endif
+int arnk_tile_lnb(bool pack, int kind, int n) {
+    const uint64_t kb = pack ? FSSB_ARNK_TILE_KB : FSSB_ARNK_UNPACK_TILE_KB;
+    return 2 * elem_bytes(kind, n) * 64 <= kb * 1024 ? 2 : 1;
+}
 
 template <bool PACK, int KIND, int W>
 cudaError_t launch_tile(int n, uint64_t count, uint64_t ld, Keys k, uint8_t* buf, cudaStream_t st) {
-    const int lnb = arnk_tile_lnb(KIND, n);
+    const int lnb = arnk_tile_lnb(PACK, KIND, n);
     const uint32_t E = 16u << lnb;
     // per buffer: the tile + 16 bytes of slack for the covering word reads,
     // rounded to 128 bytes; plus 128 bytes for the two mbarriers
