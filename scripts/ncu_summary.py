@@ -61,10 +61,14 @@ def main():
     out["algorithmic_bytes_per_unit"] = nbytes
     out["aes_blocks_per_unit"] = aes
     blocks = units * aes
-    out["aes_blocks_per_s_under_ncu"] = blocks / (out["duration_ms"] * 1e-3)
-    if "smem_wavefronts" in out:
-        out["smem_wavefronts_per_aes_block"] = out["smem_wavefronts"] / blocks
-    out["warp_instructions_per_32_blocks"] = out["instructions"] / (blocks / 32)
+    if blocks:
+        out["aes_blocks_per_s_under_ncu"] = blocks / (out["duration_ms"] * 1e-3)
+        if "smem_wavefronts" in out:
+            out["smem_wavefronts_per_aes_block"] = out["smem_wavefronts"] / blocks
+        out["warp_instructions_per_32_blocks"] = out["instructions"] / (blocks / 32)
+    else:   # byte-moving kernels (ARNK): per unit and HBM rate under ncu
+        out["warp_instructions_per_unit"] = out["instructions"] / units
+        out["dram_gb_per_s_under_ncu"] = (out["dram_read"] + out["dram_write"]) / (out["duration_ms"] * 1e-3) / 1e9
     text = json.dumps(out, indent=1)
     if len(sys.argv) > 6:
         with open(sys.argv[6], "w") as fh:
