@@ -1,0 +1,80 @@
+"""Streaming ARNK key files (keyfile.py) on the GPU: the file save_keys writes
+is byte-identical to serialize_keys(pack_keys(...)) -- itself pinned to the
+reference's containers by tests/golden -- for DCF and DPF keys at several n,
+with chunks smaller than the batch and a ragged last chunk; load_keys returns
+the same keys (both parties, or one party reading only its payload), and
+malformed files raise KeyFormatError like deserialize_keys."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU containers
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2006_04593_b200 import fss, keyfile  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+def _same(a, b):
+    for f in ("alpha_share", "seed0", "scw", "tcw", "cw_final", "sigma_cw", "leaf_cw"):
+        if hasattr(a, f):
+            x, y = getattr(a, f), getattr(b, f)
+            assert torch.equal(x.contiguous().view(torch.uint8), y.contiguous().view(torch.uint8)), f
+    assert a.party == b.party and a.n_bits == b.n_bits and a.count == b.count
+
+
+@pytest.mark.parametrize("kind,n,count,chunk", [("cmp", 32, 1000, 96), ("cmp", 8, 257, 1000),
+                                                 ("cmp", 63, 50, 7), ("eq", 32, 999, 128),
+                                                 ("eq", 64, 33, 8), ("eq", 5, 1, 1), ("cmp", 16, 0, 4)])
+def test_save_load_roundtrip(tmp_path, kind, n, count, chunk):
+    rng = np.random.default_rng(n + count)
+    keygen = fss.keygen_cmp if kind == "cmp" else fss.keygen_eq
+    _, k0, k1 = keygen(n, rng, count, device=DEV)
+    path = tmp_path / "keys.arnk"
+    nbytes = keyfile.save_keys(path, k0, k1, chunk=chunk)
+    blob = path.read_bytes()
+    assert nbytes == len(blob) and blob == fss.serialize_keys(fss.pack_keys(k0, k1))
+    r0, r1 = keyfile.load_keys(path, chunk=chunk)
+    _same(r0, k0)
+    _same(r1, k1)
+    _same(keyfile.load_keys(path, party=1, chunk=max(1, chunk // 2)), k1)
+    # the loaded keys evaluate like the originals
+    if count:
+        x = torch.from_numpy(rng.integers(0, 1 << min(n, 62), count, dtype=np.uint64).view(np.int64)).to(DEV)
+        x = x.view(torch.uint64)
+        ev = fss.eval_cmp if kind == "cmp" else fss.eval_eq
+        assert torch.equal(ev(0, r0, x).view(torch.int64), ev(0, k0, x).view(torch.int64))
+
+
+def test_golden_container_loads(tmp_path):
+    g = load_golden("fss_cmp_n32")
+    if "arnk" not in g:
+        pytest.skip("fixture without a container")
+    path = tmp_path / "g.arnk"
+    path.write_bytes(g["arnk"].tobytes())
+    r0, r1 = keyfile.load_keys(path, chunk=3)
+    b0, b1 = fss.unpack_keys(fss.deserialize_keys(g["arnk"].tobytes()), device=DEV)
+    _same(r0, b0)
+    _same(r1, b1)
+
+
+def test_malformed_files(tmp_path):
+    _, k0, k1 = fss.keygen_cmp(16, np.random.default_rng(1), 20, device=DEV)
+    path = tmp_path / "k.arnk"
+    keyfile.save_keys(path, k0, k1)
+    blob = path.read_bytes()
+    for bad in (blob[:10], b"XRNK" + blob[4:], blob[:-1], blob + b"\0", blob[:4] + b"\2" + blob[5:]):
+        path.write_bytes(bad)
+        with pytest.raises(fss.KeyFormatError):
+            keyfile.load_keys(path)
+    with pytest.raises(ValueError):
+        keyfile.load_keys(path, party=2)
+    _, w0, w1 = fss.keygen_cmp(12, np.random.default_rng(2), 4, out_bits=40, device=DEV)
+    with pytest.raises(fss.KeyFormatError):
+        keyfile.save_keys(tmp_path / "w.arnk", w0, w1)
