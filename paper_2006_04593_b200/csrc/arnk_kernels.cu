@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "../../include/ariann_fss.h"
 #include "common.cuh"
@@ -275,7 +276,8 @@ constexpr int kBatch = FSSB_ARNK_BATCH;   // row loads in flight per thread (pac
 // parameters so every record layout is compile-time.
 template <bool PACK, int KIND, int W>
 __global__ void __launch_bounds__(kArnkThreads)
-arnk_tile_kernel(int n, uint64_t count, uint64_t ld, int lnb, uint32_t stride, Keys k, uint8_t* buf) {
+arnk_tile_kernel(int n, uint64_t count, uint64_t ld, int lnb, uint32_t stride, int use_tma, Keys k,
+                 uint8_t* buf) {
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr uint32_t rec = KIND == 0 ? 17 : 17 + W;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);       // 2 mbarriers
@@ -295,7 +297,7 @@ arnk_tile_kernel(int n, uint64_t count, uint64_t ld, int lnb, uint32_t stride, K
 
     auto tile_m = [&](uint64_t t) { return (uint32_t)(count - t * E < (uint64_t)E ? count - t * E : E); };
     auto aligned = [&](uint32_t bytes, const uint8_t* gp) {
-        return (bytes & 15u) == 0 && ((uintptr_t)gp & 15u) == 0;
+        return use_tma && (bytes & 15u) == 0 && ((uintptr_t)gp & 15u) == 0;
     };
     // unpack: bring tile t into buffer b (async when aligned)
     auto fetch = [&](uint64_t t, int b) {
@@ -466,7 +468,11 @@ cudaError_t launch_tile(int n, uint64_t count, uint64_t ld, Keys k, uint8_t* buf
     if (err != cudaSuccess) return err;
     const uint64_t tiles = (count + E - 1) / E;
     const uint64_t cap = (uint64_t)sms * (per_sm > 0 ? per_sm : 1);
-    kern<<<(unsigned)(tiles < cap ? tiles : cap), kArnkThreads, smem, st>>>(n, count, ld, lnb, stride, k, buf);
+    // FSSB_ARNK_NO_TMA=1 (environment): cooperative copies instead of the bulk
+    // engine -- for compute-sanitizer initcheck, which does not see TMA writes
+    static const int use_tma = getenv("FSSB_ARNK_NO_TMA") ? 0 : 1;
+    kern<<<(unsigned)(tiles < cap ? tiles : cap), kArnkThreads, smem, st>>>(n, count, ld, lnb, stride, use_tma,
+                                                                           k, buf);
     return cudaGetLastError();
 }
 

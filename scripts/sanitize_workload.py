@@ -8,7 +8,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2006_04593_b200 import _dev, _lib, dealer, fss, nn_ops, prg, runtime  # noqa: E402
+from paper_2006_04593_b200 import _dev, _lib, dealer, fss, keyfile, nn_ops, prg, runtime, shard  # noqa: E402
 from paper_2006_04593_b200.sharing import encode_fixed, share  # noqa: E402
 
 torch.cuda.set_device(0)
@@ -20,10 +20,20 @@ for n, N in ((32, 3000), (12, 513), (63, 77)):
     fss.eval_cmp(1, k1, x, return_levels=True)
     a, e0, e1 = fss.keygen_eq(n, rng, N)
     fss.eval_eq(0, e0, x)
-    if n <= 32:
-        fss.unpack_keys(fss.deserialize_keys(fss.serialize_keys(fss.pack_keys(k0, k1))))
-        fss.unpack_keys(fss.deserialize_keys(fss.serialize_keys(fss.pack_keys(e0, e1))))
+    # ARNK tile kernels: TMA path, and the unaligned last tile (odd count) fallback
+    fss.unpack_keys(fss.deserialize_keys(fss.serialize_keys(fss.pack_keys(k0, k1))))
+    fss.unpack_keys(fss.deserialize_keys(fss.serialize_keys(fss.pack_keys(e0, e1))))
+    q0, q1 = k0.take(slice(0, N - 2)), k1.take(slice(0, N - 2))
+    fss.unpack_keys(fss.deserialize_keys(fss.serialize_keys(fss.pack_keys(q0, q1))))
 fss.keygen_eq(64, rng, 100)
+# sharded dealer (tape slices) and streaming key files
+for r in range(3):
+    shard.keygen_cmp_shard(32, np.random.default_rng(4), 1001, r, 3)
+    shard.keygen_eq_shard(40, np.random.default_rng(4), 1001, r, 3)
+a, k0, k1 = fss.keygen_cmp(32, rng, 999)
+keyfile.save_keys("/tmp/sanitize_keys.arnk", k0, k1, chunk=100)
+keyfile.load_keys("/tmp/sanitize_keys.arnk", chunk=64)
+keyfile.load_keys("/tmp/sanitize_keys.arnk", party=1, chunk=333)
 fss.keygen_cmp(16, rng, 64, out_bits=40)
 prg.expand(rng.integers(0, 256, (1000, 16), dtype=np.uint8), 3)
 seeds = torch.randint(0, 256, (1024, 16), dtype=torch.uint8, device="cuda")
