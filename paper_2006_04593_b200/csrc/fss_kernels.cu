@@ -75,6 +75,23 @@ __device__ __forceinline__ U4 sel4(bool c, U4 a, U4 b) {
     return U4{c ? a.x : b.x, c ? a.y : b.y, c ? a.z : b.z, c ? a.w : b.w};
 }
 
+// Persistent grids: CTA b owns a contiguous run of whole 32-element warp tiles
+// (runs balanced to within one tile) and its threads stride through the run.
+// Unlike a grid-wide stride, the final partial pass is then spread evenly over
+// all SMs instead of landing on the first CTAs while the last ones idle.
+struct Span {
+    uint64_t lo, hi;
+};
+
+__device__ __forceinline__ Span cta_span(uint64_t count) {
+    const uint64_t tiles = (count + 31) / 32;
+    const uint64_t t0 = tiles * blockIdx.x / gridDim.x, t1 = tiles * (blockIdx.x + 1) / gridDim.x;
+    Span sp;
+    sp.lo = 32 * t0;
+    sp.hi = 32 * t1 < count ? 32 * t1 : count;
+    return sp;
+}
+
 // ------------------------------------------------------------------ expand
 // prg.expand (prg.py:43-60): out block b = AES_{k_b}(seed) ^ seed.
 __global__ void __launch_bounds__(kKeygenThreads, 1)
@@ -83,8 +100,8 @@ expand_kernel(const uint8_t* __restrict__ seeds, uint64_t count, int blocks, uin
     fssb::fill_tables(tab);
     __syncthreads();
     const fssb::Tab tb = fssb::make_tab(tab);
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
-         e += (uint64_t)gridDim.x * blockDim.x) {
+    const Span sp = cta_span(count);
+    for (uint64_t e = sp.lo + threadIdx.x; e < sp.hi; e += blockDim.x) {
         const U4 s = ld16(seeds + 16 * e);
         uint8_t* o = out + e * 16 * blocks;
         st16(o, fssb::mmo<0, false>(tb, s, 0));
@@ -115,8 +132,8 @@ mask_stream_kernel(U4 seed, uint64_t round_idx, uint64_t blocks, uint64_t count,
     fssb::fill_tables(tab);
     __syncthreads();
     const fssb::Tab tb = fssb::make_tab(tab);
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < blocks;
-         i += (uint64_t)gridDim.x * blockDim.x) {
+    const Span sp = cta_span(blocks);
+    for (uint64_t i = sp.lo + threadIdx.x; i < sp.hi; i += blockDim.x) {
         U4 b = U4{seed.x ^ (uint32_t)round_idx, seed.y ^ (uint32_t)(round_idx >> 32),
                   seed.z ^ (uint32_t)i, seed.w ^ (uint32_t)(i >> 32)};
         b.w &= 0x7FFFFFFFu;
@@ -142,8 +159,8 @@ dpf_eval_kernel(int party, int n, uint64_t count, uint64_t ld, const uint8_t* __
     __syncthreads();
     const fssb::Tab tb = fssb::make_tab(tab);
     const uint64_t mask = ring_mask(n);
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
-         e += (uint64_t)gridDim.x * blockDim.x) {
+    const Span sp = cta_span(count);
+    for (uint64_t e = sp.lo + threadIdx.x; e < sp.hi; e += blockDim.x) {
         U4 s = ld16(seed0 + 16 * e);
         uint32_t t = party;
         const uint64_t xe = load_x(x, m_own, m_peer, n, e) & mask;
@@ -207,8 +224,8 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
     const W* __restrict__ sig_w = reinterpret_cast<const W*>(sigma_cw);
     const W* __restrict__ leaf_w = reinterpret_cast<const W*>(leaf_cw);
     constexpr int kStride = W32 ? 2 : 1;   // W-words per u64 element
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
-         e += (uint64_t)gridDim.x * blockDim.x) {
+    const Span sp = cta_span(count);
+    for (uint64_t e = sp.lo + threadIdx.x; e < sp.hi; e += blockDim.x) {
         U4 s = ld16(seed0 + 16 * e);
         uint32_t t = party;
         W acc = 0;
@@ -281,8 +298,8 @@ dpf_keygen_kernel(int n, uint64_t count, const uint64_t* __restrict__ alpha,
     __syncthreads();
     const fssb::Tab tb = fssb::make_tab(tab);
     const uint64_t mask = ring_mask(n);
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
-         e += (uint64_t)gridDim.x * blockDim.x) {
+    const Span sp = cta_span(count);
+    for (uint64_t e = sp.lo + threadIdx.x; e < sp.hi; e += blockDim.x) {
         U4 s0 = ld16(s0_init + 16 * e), s1 = ld16(s1_init + 16 * e);
         uint32_t t0 = 0, t1 = 1;
         const uint64_t al = alpha[e] & mask;
@@ -327,8 +344,8 @@ dcf_keygen_kernel(int n, int out_bits, uint64_t count, const uint64_t* __restric
     const fssb::Tab tb = fssb::make_tab(tab);
     const uint64_t nmask = ring_mask(n);
     const uint64_t mask = ring_mask(out_bits);
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
-         e += (uint64_t)gridDim.x * blockDim.x) {
+    const Span sp = cta_span(count);
+    for (uint64_t e = sp.lo + threadIdx.x; e < sp.hi; e += blockDim.x) {
         U4 s0 = ld16(s0_init + 16 * e), s1 = ld16(s1_init + 16 * e);
         uint32_t t0 = 0, t1 = 1;
         const uint64_t al = alpha[e] & nmask;
@@ -566,25 +583,29 @@ int prep_launch(K kernel, int* grid) {
 
 uint64_t ring_mask_host(int w) { return w >= 64 ? ~0ULL : ((1ULL << w) - 1); }
 
-int grid_for(uint64_t count, int sms, int threads) {
-    const uint64_t need = (count + threads - 1) / threads;
-    return (int)(need < (uint64_t)sms ? (need ? need : 1) : sms);
-}
 
-// Eval launch shape: one CTA per SM (the tables fill 128 KiB of shared
-// memory). Batches too small to give every SM kThreads threads are spread
-// over all SMs with fewer threads each instead of leaving SMs idle.
-int eval_grid(uint64_t count, int sms, int* threads) {
+// Launch shape of the AES kernels: one CTA per SM (the tables fill 128 KiB of
+// shared memory) with max_threads threads; each CTA strides through its own
+// contiguous run of elements (cta_span). Batches too small to give every SM
+// max_threads elements are spread over all SMs with fewer threads each.
+// (Trimming the thread count so the last pass over a run is full measured
+// slower than 1024 threads with a partial last pass -- profiles/r01_wave_bench.json.)
+int balanced_grid(uint64_t count, int sms, int max_threads, int* threads) {
     const uint64_t per_sm = (count + sms - 1) / sms;
-    if (per_sm >= (uint64_t)kThreads) {
-        *threads = kThreads;
+    if (per_sm >= (uint64_t)max_threads) {
+        *threads = max_threads;
         return sms;
     }
-    *threads = (int)(((per_sm + 31) / 32) * 32);
-    if (*threads < 32) *threads = 32;
-    const uint64_t grid = (count + *threads - 1) / *threads;
+    if (per_sm >= 32) {
+        *threads = (int)((per_sm + 31) / 32 * 32);
+        return sms;
+    }
+    *threads = 32;
+    const uint64_t grid = (count + 31) / 32;
     return (int)(grid < (uint64_t)sms ? (grid ? grid : 1) : sms);
 }
+
+int eval_grid(uint64_t count, int sms, int* threads) { return balanced_grid(count, sms, kThreads, threads); }
 
 int check_launch() {
     cudaError_t err = cudaGetLastError();
@@ -606,7 +627,9 @@ int fss_aes_mmo_expand(const uint8_t* seeds, uint64_t count, int out_blocks, uin
     if (count == 0) return kOk;
     int sms;
     if (int rc = prep_launch(expand_kernel, &sms)) return rc;
-    expand_kernel<<<grid_for(count, sms, kKeygenThreads), kKeygenThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+    int threads;
+    const int grid = balanced_grid(count, sms, kKeygenThreads, &threads);
+    expand_kernel<<<grid, threads, fssb::kTableBytes, (cudaStream_t)stream>>>(
         seeds, count, out_blocks, out);
     return check_launch();
 }
@@ -817,7 +840,9 @@ int fss_dpf_keygen(int n, uint64_t count, const uint64_t* alpha, const uint64_t*
     if (count == 0) return kOk;
     int sms;
     if (int rc = prep_launch(dpf_keygen_kernel, &sms)) return rc;
-    dpf_keygen_kernel<<<grid_for(count, sms, kKeygenThreads), kKeygenThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+    int threads;
+    const int grid = balanced_grid(count, sms, kKeygenThreads, &threads);
+    dpf_keygen_kernel<<<grid, threads, fssb::kTableBytes, (cudaStream_t)stream>>>(
         n, count, alpha, alpha0, s0, s1, scw, tcw, cw_final, alpha1);
     return check_launch();
 }
@@ -831,7 +856,9 @@ int fss_dcf_keygen(int n, int out_bits, uint64_t count, const uint64_t* alpha,
     if (count == 0) return kOk;
     int sms;
     if (int rc = prep_launch(dcf_keygen_kernel, &sms)) return rc;
-    dcf_keygen_kernel<<<grid_for(count, sms, kKeygenThreads), kKeygenThreads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+    int threads;
+    const int grid = balanced_grid(count, sms, kKeygenThreads, &threads);
+    dcf_keygen_kernel<<<grid, threads, fssb::kTableBytes, (cudaStream_t)stream>>>(
         n, out_bits, count, alpha, alpha0, s0, s1, scw, tcw, sigma_cw, leaf_cw, alpha1);
     return check_launch();
 }
@@ -955,7 +982,9 @@ int fss_mask_stream(uint64_t seed_lo, uint64_t seed_hi, uint64_t round_idx, uint
     const uint64_t blocks = (count + 3) / 4;
     const U4 seed = U4{(uint32_t)seed_lo, (uint32_t)(seed_lo >> 32), (uint32_t)seed_hi,
                        (uint32_t)(seed_hi >> 32)};
-    mask_stream_kernel<<<grid_for(blocks, sms, kKeygenThreads), kKeygenThreads, fssb::kTableBytes,
+    int threads;
+    const int grid = balanced_grid(blocks, sms, kKeygenThreads, &threads);
+    mask_stream_kernel<<<grid, threads, fssb::kTableBytes,
                          (cudaStream_t)stream>>>(seed, round_idx, blocks, count, ring_mask_host(n_bits),
                                                  out);
     return check_launch();

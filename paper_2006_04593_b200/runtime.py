@@ -456,6 +456,20 @@ def run_session(party: int, transport, program):
     return result, session.ledger
 
 
+_PARTY_STREAMS = {}
+
+
+def _party_streams(dev) -> list:
+    """The two party threads' CUDA streams on ``dev``, created once per device:
+    the caching allocator keeps its free blocks per stream, so fresh streams on
+    every call would make each online run cudaMalloc its buffers anew (measured:
+    4 cudaMalloc per ReLU run, 8-430 ms online instead of ~3.5 ms)."""
+    key = str(dev)
+    if key not in _PARTY_STREAMS:
+        _PARTY_STREAMS[key] = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    return _PARTY_STREAMS[key]
+
+
 def run_local_pair(program0, program1=None, device=None):
     """Two programs over the in-process transport, one thread per party
     (runtime.py:285-311). Each party thread runs on its own CUDA stream of
@@ -471,7 +485,7 @@ def run_local_pair(program0, program1=None, device=None):
         dev = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
         parent = torch.cuda.current_stream(dev)
-        streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+        streams = _party_streams(dev)
         for s in streams:
             s.wait_stream(parent)
 
