@@ -26,6 +26,22 @@ def default_device(device=None) -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_SIDE_STREAMS = {}
+
+
+def side_streams(device: torch.device, k: int = 2) -> list:
+    """k CUDA side streams of ``device`` for the calling thread, created once
+    and reused (stream creation per call costs time, and the caching allocator
+    pools free blocks per stream)."""
+    import threading
+    key = (str(device), threading.get_ident())
+    got = _SIDE_STREAMS.get(key, [])
+    while len(got) < k:
+        got.append(torch.cuda.Stream(device))
+    _SIDE_STREAMS[key] = got
+    return got[:k]
+
+
 def stream_handle(device: torch.device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 

@@ -513,7 +513,7 @@ def _run_eval(launch, xt, host, count: int, dev, host_launch=None):
     # device scratch on the current stream; the side streams wait for it and the
     # current stream waits for them, so the allocator cannot recycle it early
     scratch = torch.empty((2, 2 * chunk), dtype=torch.uint64, device=dev)
-    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    streams = _dev.side_streams(dev, 2)
     for st in streams:
         st.wait_stream(cur)
     if host == "torch_pinned":

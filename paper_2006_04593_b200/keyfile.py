@@ -23,7 +23,6 @@ from __future__ import annotations
 
 import os
 
-import numpy as np
 import torch
 
 from . import _dev, _lib, fss
@@ -78,7 +77,7 @@ def save_keys(path, k0, k1, chunk: int = CHUNK) -> int:
     chunk = max(1, min(chunk, max(count, 1)))
     pinned = [torch.empty(chunk * elem, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
     done = [None, None]
-    side = torch.cuda.Stream(dev)
+    side = _dev.side_streams(dev, 1)[0]
     written = 0
     with open(path, "wb") as fh:
         fh.write(_header(kind, n, count))
