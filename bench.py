@@ -330,35 +330,55 @@ def measure_pair_protocol(dev, xdev, rank, barrier, max_over_ranks, M=1 << 22, r
     return out
 
 
-def measure_gather(out0, out1, total, rank, barrier, max_over_ranks, reps=5):
-    """The output collective of SURVEY §8e: both parties' shares of every
-    rank's slice to rank 0 at the ring's wire width (shard.gather_ring: 4 B per
-    element per party at n = 32), then reconstructed there. Max over ranks of
-    the wall time per gather of both parties."""
+def measure_gather(k0, k1, x, total, rank, barrier, max_over_ranks, reps=5):
+    """The output collective of SURVEY §8e, three ways, per step of BOTH parties'
+    evaluation of this rank's slice (max over ranks of the wall time):
+    * eval_only   -- the two eval launches, shares stay local (the `value` step);
+    * nccl_gather -- + both parties' shares to rank 0 at wire width
+                     (shard.gather_ring: 4 B per element per party, NCCL);
+    * peer_fused  -- the eval kernels store their shares straight into rank 0's
+                     result buffer through CUDA IPC peer memory
+                     (shard.PeerGather, fss.eval_cmp(out=...)), then finish().
+    Rank 0 checks that both gathers reconstruct to bits."""
     import torch
 
-    from paper_2006_04593_b200 import shard
+    from paper_2006_04593_b200 import fss, shard
 
-    def once():
-        g0 = shard.gather_ring(out0, N_BITS, total, dst=0)
-        g1 = shard.gather_ring(out1, N_BITS, total, dst=0)
-        return g0, g1
+    def eval_only():
+        return fss.eval_cmp(0, k0, x), fss.eval_cmp(1, k1, x)
 
-    g0, g1 = once()
-    if rank == 0:   # reconstruction of the gathered shares: one bit per comparison
-        rec = (g0.view(torch.int64) + g1.view(torch.int64)) & 0xFFFFFFFF
-        assert bool(((rec == 0) | (rec == 1)).all()), "gathered shares do not reconstruct to bits"
-    del g0, g1
-    barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        once()
-    torch.cuda.synchronize()
-    t = max_over_ranks((time.perf_counter() - t0) / reps)
-    nbytes = 2 * total * 4
-    return {"elements": total, "ms_per_gather": t * 1e3, "bytes_to_rank0": nbytes,
-            "gb_per_s_into_rank0": nbytes / t / 1e9}
+    def nccl():
+        y0, y1 = eval_only()
+        return shard.gather_ring(y0, N_BITS, total, dst=0), shard.gather_ring(y1, N_BITS, total, dst=0)
+
+    g = shard.PeerGather(total, slots=2, dst=0)
+
+    def fused():
+        fss.eval_cmp(0, k0, x, out=g.out(0))
+        fss.eval_cmp(1, k1, x, out=g.out(1))
+        return g.finish()
+
+    def check(r0, r1):
+        if rank == 0:
+            rec = (r0.view(torch.int64) + r1.view(torch.int64)) & 0xFFFFFFFF
+            assert bool(((rec == 0) | (rec == 1)).all()), "gathered shares do not reconstruct to bits"
+
+    check(*nccl())
+    res = fused()
+    if rank == 0:
+        check(res[0], res[1])
+    out = {"elements": total, "bytes_to_rank0_wire": 2 * total * 4, "bytes_to_rank0_fused": 2 * total * 8}
+    for name, fn in (("eval_only", eval_only), ("nccl_gather", nccl), ("peer_fused", fused)):
+        fn()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+        out[f"{name}_ms_per_step"] = max_over_ranks((time.perf_counter() - t0) / reps) * 1e3
+    g.close()
+    return out
 
 
 def run_ours(args, ws, rank, local):
@@ -466,7 +486,7 @@ def run_ours(args, ws, rank, local):
                                                                    max_over_ranks)
     if ws >= 2 and not args.no_secondary:
         secondary = dict(secondary or {})
-        secondary["output_gather"] = measure_gather(out0, out1, N * ws, rank, barrier,
+        secondary["output_gather"] = measure_gather(k0, k1, x, N * ws, rank, barrier,
                                                     max_over_ranks)
     del out0, out1, rec
 

@@ -491,7 +491,21 @@ PIPELINE_MIN = 1 << 21
 PIPELINE_CHUNK = 1 << 20
 
 
-def _run_eval(launch, xt, host, count: int, dev, host_launch=None):
+def _check_out(out, count: int, dev):
+    """A caller-provided destination of the shares: ``count`` u64 words of device
+    memory on ``dev`` (a torch tensor, or e.g. a peer-mapped shard.PeerGather slot)."""
+    if out is None:
+        return None
+    if not getattr(out, "is_cuda", False) or torch.device(out.device) != dev:
+        raise ValueError(f"out must be device memory on {dev}")
+    if out.dtype not in (torch.uint64, torch.int64) or out.numel() != count:
+        raise ValueError(f"out must hold {count} 64-bit words")
+    if isinstance(out, torch.Tensor) and not out.is_contiguous():
+        raise ValueError("out must be contiguous")
+    return out
+
+
+def _run_eval(launch, xt, host, count: int, dev, host_launch=None, out=None):
     """Run the evaluation over [0, count).
 
     Device input: ``launch(lo, hi, x_dev, out_dev, stream)`` once on the current
@@ -502,6 +516,11 @@ def _run_eval(launch, xt, host, count: int, dev, host_launch=None):
     Pinned torch input returns a pinned host tensor; numpy input (pageable) is
     staged through pinned slots inside the call and returns a numpy array."""
     big = count >= PIPELINE_MIN and host_launch is not None
+    if out is not None:
+        if host:
+            raise ValueError("out= needs a device input x (device in, device out)")
+        launch(0, count, xt, out, _dev.stream_handle(dev))
+        return out
     if not big or host not in ("torch_pinned", "numpy"):
         if host in ("torch_pinned", "numpy"):
             xt = (torch.from_numpy(xt) if host == "numpy" else xt).to(dev, non_blocking=True)
@@ -543,10 +562,12 @@ def _prep_x(x, count: int, n: int, dev):
     return _broadcast_x(x, count, n, dev)
 
 
-def eval_eq(party: int, k: EqKeyBatch, x):
-    """Per-party share of 1[x == alpha] (fss.py:357-377) via fss_dpf_eval."""
+def eval_eq(party: int, k: EqKeyBatch, x, out=None):
+    """Per-party share of 1[x == alpha] (fss.py:357-377) via fss_dpf_eval.
+    ``out``: as for eval_cmp."""
     k.validate()
     n, count, dev = k.n_bits, k.count, k.device
+    out = _check_out(out, count, dev)
     xt, host = _prep_x(x, count, n, dev)
     ld = _eval_operands(k, ("tcw",))
     seed0, cw_final = k.seed0.contiguous(), k.cw_final.contiguous()
@@ -562,16 +583,22 @@ def eval_eq(party: int, k: EqKeyBatch, x):
             _lib.call("fss_dpf_eval_host", int(party), n, count, ld, _dev.ptr(seed0),
                       _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(cw_final), xh, oh,
                       _dev.ptr(xs), _dev.ptr(os_), chunk, stage, sa, sb)
-    return _run_eval(launch, xt, host, count, dev, host_launch)
+    return _run_eval(launch, xt, host, count, dev, host_launch, out)
 
 
-def eval_cmp(party: int, k: CmpKeyBatch, x, return_levels: bool = False):
+def eval_cmp(party: int, k: CmpKeyBatch, x, return_levels: bool = False, out=None):
     """Per-party share of 1[x <= alpha] (fss.py:380-426) via fss_dcf_eval.
 
     With return_levels the per-level output terms are also returned,
-    shape (n+1, count); at most one level reconstructs to 1."""
+    shape (n+1, count); at most one level reconstructs to 1. ``out`` (device
+    input only, extension): write the shares into this device buffer of count
+    u64 words -- e.g. a slot of another GPU's gather buffer (shard.PeerGather),
+    so the kernel's stores are the output collective."""
     k.validate()
     n, count, dev = k.n_bits, k.count, k.device
+    out = _check_out(out, count, dev)
+    if out is not None and return_levels:
+        raise ValueError("out= and return_levels are exclusive")
     xt, host = _prep_x(x, count, n, dev)
     ld = _eval_operands(k, ("tcw", "sigma_cw", "leaf_cw"))
     seed0 = k.seed0.contiguous()
@@ -601,7 +628,7 @@ def eval_cmp(party: int, k: CmpKeyBatch, x, return_levels: bool = False):
                       _dev.ptr(seed0), _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(k.sigma_cw),
                       _dev.ptr(k.leaf_cw), xh, oh, _dev.ptr(xs), _dev.ptr(os_), chunk, stage,
                       sa, sb)
-    return _run_eval(launch, xt, host, count, dev, host_launch)
+    return _run_eval(launch, xt, host, count, dev, host_launch, out)
 
 
 # ---------------------------------------------------------------------------

@@ -18,7 +18,10 @@ collective. This module supplies the two pieces around that:
   collective of §8e -- the evaluated shares of every slice to rank ``dst`` (or to
   all ranks) for reconstruction; ``gather_ring`` ships them at the ring's wire
   width (4 B per element for n <= 32, the reference's ``pack_ring``,
-  sharing.py:191-207).
+  sharing.py:191-207) over NCCL.
+* ``PeerGather``: the same gather fused into the evaluation -- every rank's eval
+  kernel stores its shares straight into rank dst's result buffer through CUDA
+  IPC peer memory (``fss.eval_cmp(..., out=gather.out(party))``).
 
 The masked-message exchange between the two parties is the other collective and
 lives in ``runtime`` (``DistTransport`` over NCCL, ``PeerTransport`` over peer
@@ -131,3 +134,90 @@ def gather_ring(values: torch.Tensor, n_bits: int, total: int, dst=0, group=None
     if got is None:
         return None
     return sharing.unpack_ring(got, n_bits) if got.is_cuda else got
+
+
+class _RawCuda:
+    """__cuda_array_interface__ view of raw device memory (zero-copy torch view)."""
+
+    def __init__(self, ptr: int, shape, typestr: str = "<i8"):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+class PeerGather:
+    """The output gather fused with the evaluation over peer memory.
+
+    Rank ``dst`` allocates a (slots, total) u64 result buffer -- one row per
+    output, e.g. slot 0 / 1 for the two parties' shares -- and exports it with
+    CUDA IPC; every rank maps it. ``out(slot)`` is this rank's [lo, hi) window
+    of row ``slot``: passed as ``out=`` to ``fss.eval_cmp`` / ``fss.eval_eq``,
+    it makes the evaluation kernel's own stores land in rank dst's HBM (NVLink /
+    NVSwitch peer stores; the same HBM when the ranks share a GPU), so there is
+    no separate gather collective and no staging copy. ``finish()`` orders the
+    writes (stream sync on every rank, then a barrier) and returns the
+    (slots, total) u64 tensor on rank dst -- a view valid until ``close()`` --
+    and None elsewhere."""
+
+    def __init__(self, total: int, slots: int = 2, dst: int = 0, group=None, device=None):
+        import ctypes
+
+        from . import _lib
+        self._lib, self.group = _lib, group
+        self.rank, self.world = _rank_world(None, None, group)
+        self.total, self.slots, self.dst = int(total), int(slots), int(dst)
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self.lo, self.hi = shard_bounds(self.total, self.rank, self.world)
+        hb = _lib.load().fss_ipc_handle_bytes()
+        handle = torch.zeros(hb, dtype=torch.uint8)
+        self._owned = None
+        with torch.cuda.device(self.device):
+            if self.rank == self.dst:
+                ptr = ctypes.c_void_p()
+                _lib.call("fss_ipc_alloc", max(8 * self.slots * self.total, 16), ctypes.byref(ptr))
+                self._owned = self.base = ptr.value
+                buf = (ctypes.c_uint8 * hb)()
+                _lib.call("fss_ipc_get_handle", ptr, buf)
+                handle = torch.tensor(list(buf), dtype=torch.uint8)
+            comm = handle.to(self.device) if dist.get_backend(group) == "nccl" else handle
+            dist.broadcast(comm, src=self.dst, group=group)
+            if self.rank != self.dst:
+                raw = (ctypes.c_uint8 * hb)(*comm.cpu().tolist())
+                ptr = ctypes.c_void_p()
+                _lib.call("fss_ipc_open_handle", raw, ctypes.byref(ptr))
+                self.base = ptr.value
+        self._closed = False
+
+    def out(self, slot: int):
+        """This rank's window of row ``slot`` as a device buffer for ``out=``."""
+        from .runtime import PeerBuffer
+        if not 0 <= slot < self.slots:
+            raise ValueError(f"slot {slot} outside [0, {self.slots})")
+        ptr = self.base + 8 * (slot * self.total + self.lo)
+        return PeerBuffer(ptr, self.hi - self.lo, torch.uint64, self.device)
+
+    def _barrier(self):
+        dist.barrier(group=self.group) if self.group is not None else dist.barrier()
+
+    def finish(self):
+        """Every rank's stores are complete and visible: the (slots, total) u64
+        result on rank dst, None elsewhere."""
+        torch.cuda.current_stream(self.device).synchronize()
+        self._barrier()
+        if self.rank != self.dst:
+            return None
+        return torch.as_tensor(_RawCuda(self.base, (self.slots, self.total)),
+                               device=self.device).view(torch.uint64)
+
+    def close(self):
+        import ctypes
+        if self._closed:
+            return
+        self._closed = True
+        torch.cuda.current_stream(self.device).synchronize()
+        self._barrier()                      # nobody writes or reads any more
+        with torch.cuda.device(self.device):
+            if self.rank == self.dst:
+                self._lib.call("fss_ipc_free", ctypes.c_void_p(self._owned))
+            else:
+                self._lib.call("fss_ipc_close_handle", ctypes.c_void_p(self.base))

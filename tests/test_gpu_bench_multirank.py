@@ -43,4 +43,6 @@ def test_two_rank_bench_contract():
     assert pp["nccl"]["comparisons_per_s_per_pair"] > 0
     assert pp["peer_memory"]["comparisons_per_s_per_pair"] > 0
     g = d["secondary"]["output_gather"]   # both parties' shares of 2 x 2^18 elements to rank 0
-    assert g["elements"] == 2 << 18 and g["bytes_to_rank0"] == 2 * (2 << 18) * 4
+    assert g["elements"] == 2 << 18 and g["bytes_to_rank0_wire"] == 2 * (2 << 18) * 4
+    assert g["eval_only_ms_per_step"] > 0 and g["nccl_gather_ms_per_step"] > 0
+    assert g["peer_fused_ms_per_step"] > 0

@@ -181,3 +181,67 @@ def test_two_process_sharded_keygen_eval_gather():
         p.join(timeout=60)
     assert res == {0: True, 1: True}
     assert all(p.exitcode == 0 for p in procs)
+
+
+def _worker_peer(rank, port, total, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        x = np.random.default_rng(8).integers(0, 1 << 32, total, dtype=np.uint64)
+        alpha, k0, k1 = shard.keygen_cmp_shard(32, np.random.default_rng(4), total, device=DEV)
+        lo, hi = shard.shard_bounds(total, rank, 2)
+        xs = torch.from_numpy(x[lo:hi].view(np.int64)).to(DEV).view(torch.uint64)
+        g = shard.PeerGather(total, slots=2, dst=1)
+        for rnd in range(2):                  # the buffer is reusable round after round
+            fss.eval_cmp(0, k0, xs, out=g.out(0))
+            fss.eval_cmp(1, k1, xs, out=g.out(1))
+            res = g.finish()
+        ok = True
+        if rank == 1:
+            fa, f0, f1 = fss.keygen_cmp(32, np.random.default_rng(4), total, device=DEV)
+            xd = torch.from_numpy(x.view(np.int64)).to(DEV).view(torch.uint64)
+            w0, w1 = fss.eval_cmp(0, f0, xd), fss.eval_cmp(1, f1, xd)
+            ok = (tuple(res.shape) == (2, total)
+                  and torch.equal(res[0].view(torch.int64), w0.view(torch.int64))
+                  and torch.equal(res[1].view(torch.int64), w1.view(torch.int64)))
+        else:
+            ok = res is None
+        g.close()
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_process_peer_gather_fused_with_eval():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker_peer, args=(r, port, 30001, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}
+    assert all(p.exitcode == 0 for p in procs)
+
+
+def test_eval_out_argument():
+    _, k0, _ = fss.keygen_cmp(32, np.random.default_rng(2), 1000, device=DEV)
+    _, e0, _ = fss.keygen_eq(32, np.random.default_rng(2), 1000, device=DEV)
+    x = torch.arange(1000, device=DEV).view(torch.uint64)
+    buf = torch.empty(1000, dtype=torch.uint64, device=DEV)
+    assert fss.eval_cmp(0, k0, x, out=buf) is buf
+    assert torch.equal(buf.view(torch.int64), fss.eval_cmp(0, k0, x).view(torch.int64))
+    assert fss.eval_eq(0, e0, x, out=buf) is buf
+    assert torch.equal(buf.view(torch.int64), fss.eval_eq(0, e0, x).view(torch.int64))
+    with pytest.raises(ValueError):
+        fss.eval_cmp(0, k0, x, out=buf[:999])
+    with pytest.raises(ValueError):
+        fss.eval_cmp(0, k0, np.zeros(1000, dtype=np.uint64), out=buf)   # host input
+    with pytest.raises(ValueError):
+        fss.eval_cmp(0, k0, x, out=torch.empty(1000, dtype=torch.uint64))  # host buffer
+    with pytest.raises(ValueError):
+        fss.eval_cmp(0, k0, x, return_levels=True, out=buf)
