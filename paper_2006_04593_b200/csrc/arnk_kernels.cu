@@ -435,6 +435,169 @@ arnk_tile_kernel(int n, uint64_t count, uint64_t ld, int lnb, uint32_t stride, i
     if (PACK && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ---- pack with asynchronously staged key rows ------------------------------
+// The pack kernel above loads each thread's key rows with plain loads, so its
+// warps stall on HBM latency and at the tile barriers (ncu r01f: long
+// scoreboard + barrier stalls, 27 % issue-active). Here every row segment of
+// tile j+1 -- scw, tcw, sigma, leaf, alpha, seed, cw_final -- is copied into
+// a shared-memory staging buffer with cp.async (LDGSTS: global -> shared, no
+// register round trip, all in flight at once) while the threads assemble tile
+// j from the other staging buffer; the assembled payload leaves through the
+// TMA bulk store as before. Needs ld % 4 == 0 (4-byte cp.async of the tcw
+// rows, tcw / scw / seed bases aligned); other layouts take the kernel above.
+__device__ __forceinline__ void cp_async(void* dst, const void* src, int bytes) {
+    const uint32_t d = smem_u32(dst);
+    if (bytes == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+    else if (bytes == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+
+struct Stage {   // byte offsets of the row blocks inside one staging buffer (E elements)
+    uint32_t scw, sig, leaf, alpha, cwf, seed, tcw, bytes;
+};
+
+__host__ __device__ __forceinline__ Stage stage_layout(int kind, int n, uint32_t E) {
+    Stage g;
+    g.scw = 0;
+    g.sig = g.scw + (uint32_t)n * E * 16;
+    g.leaf = g.sig + (kind == 1 ? (uint32_t)n * E * 8 : 0);
+    g.alpha = g.leaf + (kind == 1 ? (uint32_t)(n + 1) * E * 8 : 0);
+    g.cwf = g.alpha + E * 8;
+    g.seed = g.cwf + (kind == 0 ? E * 8 : 0);
+    g.tcw = g.seed + E * 16;
+    g.bytes = (g.tcw + (uint32_t)n * E + 127) / 128 * 128;
+    return g;
+}
+
+template <int KIND, int W>
+__global__ void __launch_bounds__(kArnkThreads)
+arnk_pack_async_kernel(int n, uint64_t count, uint64_t ld, int lnb, uint32_t stride, uint32_t sstride,
+                       int use_tma, Keys k, uint8_t* buf) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    constexpr uint32_t rec = KIND == 0 ? 17 : 17 + W;
+    uint8_t* tiles_base = smem;                    // 2 payload buffers
+    uint8_t* stage_base = smem + 2 * stride;       // 2 staging buffers
+    const uint32_t E = 16u << lnb;
+    const uint32_t EB = (uint32_t)elem_bytes(KIND, n);
+    const uint32_t tail = W + 16 + n * rec;
+    const int d_lv = row_step_log2(rec), d_leaf = row_step_log2(W);
+    const Stage G = stage_layout(KIND, n, E);
+    const uint64_t tiles = (count + E - 1) / E;
+    auto tile_m = [&](uint64_t t) { return (uint32_t)(count - t * E < (uint64_t)E ? count - t * E : E); };
+
+    // issue the copies of tile t's key rows into staging buffer b (one group)
+    auto stage_in = [&](uint64_t t, int b) {
+        uint8_t* S = stage_base + b * sstride;
+        const uint64_t e0 = t * E;
+        const uint32_t m = tile_m(t);
+        const uint32_t q16 = m, q8 = m;                     // 16-B / 8-B pieces per row
+        // scw rows (16 B per key) and seeds
+        for (uint32_t i = threadIdx.x; i < (uint32_t)n * q16; i += kArnkThreads) {
+            const uint32_t row = i / q16, e = i - row * q16;
+            cp_async(S + G.scw + (row * E + e) * 16, k.scw + 16 * ((uint64_t)row * ld + e0 + e), 16);
+        }
+        for (uint32_t e = threadIdx.x; e < m; e += kArnkThreads) {
+            cp_async(S + G.seed + e * 16, k.seed0 + 16 * (e0 + e), 16);
+            cp_async(S + G.alpha + e * 8, k.alpha_share + e0 + e, 8);
+            if (KIND == 0) cp_async(S + G.cwf + e * 8, k.cw_final + e0 + e, 8);
+        }
+        if (KIND == 1) {
+            // sigma / leaf rows (8 B per key): 16-byte pieces of key pairs when
+            // the rows are 16-byte aligned (ld even; e0 is a multiple of 16),
+            // the odd last key of a ragged tile on its own
+            const bool a16 = !(ld & 1) && !(((uintptr_t)k.sigma_cw | (uintptr_t)k.leaf_cw) & 15);
+            const uint32_t pairs = a16 ? m / 2 : 0, singles = m - 2 * pairs;
+            const uint32_t q = pairs + singles;
+            for (uint32_t i = threadIdx.x; i < (uint32_t)(2 * n + 1) * q; i += kArnkThreads) {
+                const uint32_t r = i / q, c = i - r * q;
+                const bool leaf = r >= (uint32_t)n;
+                const uint32_t row = leaf ? r - n : r;
+                const uint32_t e = c < pairs ? 2 * c : 2 * pairs + (c - pairs);
+                const uint64_t* src = (leaf ? k.leaf_cw : k.sigma_cw) + (uint64_t)row * ld + e0 + e;
+                cp_async(S + (leaf ? G.leaf : G.sig) + (row * E + e) * 8, src, c < pairs ? 16 : 8);
+            }
+        }
+        // tcw rows: one 16-byte piece per 16 keys when ld % 16 == 0, else
+        // 4-byte pieces (ld % 4 == 0); a ragged tail of the last tile by plain
+        // byte copies
+        const uint32_t pw = ((ld & 15) || ((uintptr_t)k.tcw & 15)) ? 4 : 16;
+        const uint32_t qw = m / pw;
+        for (uint32_t i = threadIdx.x; i < (uint32_t)n * qw; i += kArnkThreads) {
+            const uint32_t row = i / qw, w = i - row * qw;
+            cp_async(S + G.tcw + row * E + pw * w, k.tcw + (uint64_t)row * ld + e0 + pw * w, (int)pw);
+        }
+        const uint32_t rag = m - pw * qw;
+        for (uint32_t i = threadIdx.x; i < (uint32_t)n * rag; i += kArnkThreads) {
+            const uint32_t row = i / rag, e = pw * qw + (i - row * rag);
+            S[G.tcw + row * E + e] = k.tcw[(uint64_t)row * ld + e0 + e];
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+    int j = 0;
+    if (blockIdx.x < tiles) stage_in(blockIdx.x, 0);
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, j++) {
+        const int cur = j & 1;
+        uint8_t* tile = tiles_base + cur * stride;
+        const uint8_t* S = stage_base + cur * sstride;
+        const uint32_t m = tile_m(t);
+        uint8_t* gp = buf + t * E * EB;
+        const bool async_io = use_tma && ((m * EB) & 15u) == 0 && ((uintptr_t)gp & 15u) == 0;
+        // staging buffer cur^1 was consumed by tile j-1 (barrier at its end)
+        const uint64_t tn = t + gridDim.x;
+        if (tn < tiles) {
+            stage_in(tn, cur ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");   // tile j's rows have landed
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        // the bulk store issued from this payload buffer two tiles ago has read it
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncthreads();
+        const uint32_t items = pair_items((uint32_t)n, lnb, d_lv);
+        for (uint32_t idx = threadIdx.x; idx < items; idx += kArnkThreads) {
+            const Item it = pair_item(idx, lnb, d_lv);
+            if (it.row >= (uint32_t)n || it.e >= m) continue;
+            const uint32_t so = it.e * EB + W + 16 + it.row * rec;
+            const uint4 v = *reinterpret_cast<const uint4*>(S + G.scw + (it.row * E + it.e) * 16);
+            const uint32_t f = S[G.tcw + it.row * E + it.e];
+            const uint64_t sg = KIND == 1 ? *reinterpret_cast<const uint64_t*>(S + G.sig + (it.row * E + it.e) * 8)
+                                          : 0;
+            const uint32_t R[7] = {v.x, v.y, v.z, v.w, f | ((uint32_t)sg << 8), (uint32_t)(sg >> 24),
+                                   (uint32_t)(sg >> 56)};
+            sput_stream<rec>(tile, so, R);
+        }
+        for (uint32_t e = threadIdx.x; e < m; e += kArnkThreads) {
+            const uint32_t so = e * EB;
+            sput_u64<W>(tile, so, *reinterpret_cast<const uint64_t*>(S + G.alpha + e * 8));
+            sput16(tile, so + W, *reinterpret_cast<const uint4*>(S + G.seed + e * 16));
+            if (KIND == 0) sput_u64<W>(tile, so + tail, *reinterpret_cast<const uint64_t*>(S + G.cwf + e * 8));
+        }
+        if (KIND == 1) {
+            const uint32_t leaf_items = pair_items((uint32_t)n + 1, lnb, d_leaf);
+            for (uint32_t idx = threadIdx.x; idx < leaf_items; idx += kArnkThreads) {
+                const Item it = pair_item(idx, lnb, d_leaf);
+                if (it.row > (uint32_t)n || it.e >= m) continue;
+                sput_u64<W>(tile, it.e * EB + tail + it.row * W,
+                            *reinterpret_cast<const uint64_t*>(S + G.leaf + (it.row * E + it.e) * 8));
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();   // payload assembled; staging buffer cur fully read
+        if (async_io) {
+            if (threadIdx.x == 0) bulk_store(gp, tile, m * EB);
+        } else {
+            copy_range(gp, tile, (uint64_t)m * EB);
+            if (threadIdx.x == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // Tile of E = 16 << lnb elements, two tile buffers per CTA. Unpack: 64
 // elements whenever the two buffers fit 110 KiB (cmp n = 32: 2 x 52.7 KB, two
 // CTAs per SM); pack: 64 only up to 100 KiB, i.e. 32 for cmp n = 32 (four
@@ -451,8 +614,48 @@ int arnk_tile_lnb(bool pack, int kind, int n) {
     return 2 * elem_bytes(kind, n) * 64 <= kb * 1024 ? 2 : 1;
 }
 
+#ifndef FSSB_ARNK_ASYNC_PACK
+#define FSSB_ARNK_ASYNC_PACK 1
+#endif
+
+template <int KIND, int W>
+cudaError_t launch_pack_async(int n, uint64_t count, uint64_t ld, Keys k, uint8_t* buf, cudaStream_t st) {
+    // 32-key tiles when two CTAs (2 payload + 2 staging buffers each) fit an
+    // SM, else 16-key tiles: the assembly needs the warps of several CTAs
+    // (cmp n = 32: 32 keys = 122 KB per CTA, one CTA per SM measured 30 %
+    // slower than 16 keys at three CTAs per SM)
+    auto smem_for = [&](uint32_t E) {
+        return 2 * (size_t)((elem_bytes(KIND, n) * E + 16 + 127) / 128 * 128) +
+               2 * (size_t)stage_layout(KIND, n, E).bytes;
+    };
+    const int lnb = 2 * smem_for(32) <= 200 * 1024 ? 1 : 0;
+    const uint32_t E = 16u << lnb;
+    const uint32_t stride = (uint32_t)((elem_bytes(KIND, n) * E + 16 + 127) / 128 * 128);
+    const uint32_t sstride = stage_layout(KIND, n, E).bytes;
+    const size_t smem = smem_for(E);
+    int dev = 0, sms = 0, per_sm = 1;
+    auto kern = arnk_pack_async_kernel<KIND, W>;
+    cudaError_t err = cudaGetDevice(&dev);
+    if (err == cudaSuccess) err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (err == cudaSuccess) err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err == cudaSuccess) err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kArnkThreads, smem);
+    if (err != cudaSuccess) return err;
+    const uint64_t tiles = (count + E - 1) / E;
+    const uint64_t cap = (uint64_t)sms * (per_sm > 0 ? per_sm : 1);
+    static const int use_tma = getenv("FSSB_ARNK_NO_TMA") ? 0 : 1;
+    kern<<<(unsigned)(tiles < cap ? tiles : cap), kArnkThreads, smem, st>>>(n, count, ld, lnb, stride, sstride,
+                                                                           use_tma, k, buf);
+    return cudaGetLastError();
+}
+
 template <bool PACK, int KIND, int W>
 cudaError_t launch_tile(int n, uint64_t count, uint64_t ld, Keys k, uint8_t* buf, cudaStream_t st) {
+    // cp.async needs naturally aligned pieces: tcw rows 4-byte aligned, scw /
+    // seed rows 16-byte aligned (sigma / leaf pick 16 or 8 in the kernel)
+    if (PACK && FSSB_ARNK_ASYNC_PACK && ld % 4 == 0 && !((uintptr_t)k.tcw & 3) &&
+        !(((uintptr_t)k.scw | (uintptr_t)k.seed0) & 15) && !((uintptr_t)k.alpha_share & 7) &&
+        2 * (elem_bytes(KIND, n) * 16 + 144) + 2 * stage_layout(KIND, n, 16).bytes <= 220 * 1024)
+        return launch_pack_async<KIND, W>(n, count, ld, k, buf, st);
     const int lnb = arnk_tile_lnb(PACK, KIND, n);
     const uint32_t E = 16u << lnb;
     // per buffer: the tile + 16 bytes of slack for the covering word reads,

@@ -24,10 +24,7 @@ VDIR = os.path.join(ROOT, "build", "variants")
 # variant name -> compile-time defines (the shipped library is "main")
 VARIANTS = {
     "naive": ["FSSB_ARNK_NAIVE=1"],
-    "batch2": ["FSSB_ARNK_BATCH=2"],
-    "batch8": ["FSSB_ARNK_BATCH=8"],
-    "tile64": ["FSSB_ARNK_TILE_KB=110"],
-    "tile64_b8": ["FSSB_ARNK_TILE_KB=110", "FSSB_ARNK_BATCH=8"],
+    "sync_pack": ["FSSB_ARNK_ASYNC_PACK=0"],
 }
 
 

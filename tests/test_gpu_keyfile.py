@@ -78,3 +78,23 @@ def test_malformed_files(tmp_path):
     _, w0, w1 = fss.keygen_cmp(12, np.random.default_rng(2), 4, out_bits=40, device=DEV)
     with pytest.raises(fss.KeyFormatError):
         keyfile.save_keys(tmp_path / "w.arnk", w0, w1)
+
+
+@pytest.mark.parametrize("kind,n,count", [("cmp", 32, 1000), ("cmp", 32, 997), ("eq", 32, 1002),
+                                          ("cmp", 12, 515), ("eq", 7, 333), ("cmp", 63, 100)])
+def test_pack_of_column_views_matches_full_payload(kind, n, count):
+    """ARNK pack of column views (odd / even offsets, so the kernels' aligned
+    async-copy paths and their fallbacks both run) equals the same byte range
+    of the full batch's payload; unpack restores the view's keys."""
+    keygen = fss.keygen_cmp if kind == "cmp" else fss.keygen_eq
+    _, k0, _ = keygen(n, np.random.default_rng(count), count, device=DEV)
+    full = fss._pack_device(k0)
+    elem = full.shape[1]
+    for lo, hi in ((0, count), (1, count), (2, count - 3), (3, 40), (16, count - 1), (17, 18)):
+        v = k0.take(slice(lo, hi))
+        got = fss._pack_device(v)
+        assert torch.equal(got, full[lo:hi]), (lo, hi)
+        back = fss._unpack(fss.KIND_CMP if kind == "cmp" else fss.KIND_EQ, 0, n, hi - lo,
+                           got.reshape(-1), DEV)
+        _same(back, k0.take(np.arange(lo, hi)))
+    assert elem == (fss.cmp_elem_bytes(n) if kind == "cmp" else fss.eq_elem_bytes(n))
