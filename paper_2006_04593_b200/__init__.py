@@ -6,7 +6,7 @@ Python API. See DESIGN.md.
 
 from . import _lib
 
-__all__ = ["prg", "fss", "ring", "sharing", "runtime", "beaver", "nn_ops", "dealer"]
+__all__ = ["prg", "fss", "ring", "sharing", "runtime", "beaver", "nn_ops", "dealer", "keyfile", "shard"]
 __version__ = "0.1.0"
 
 
