@@ -13,7 +13,10 @@ for party 0 and party 1 over every element (two kernel launches).
 
 `e2e` = the same metric through the public drop-in API with host buffers: per
 step eval_cmp for both parties on a pinned host x (keys dealt beforehand and
-resident in HBM, as in `value`), shares copied back to pinned host memory.
+resident in HBM, as in `value`), the shares returned in pinned host memory.
+The host path is zero-copy: the eval kernel reads x from and stores the shares
+to the pinned host buffers itself (UVA, over PCIe), so the 2 x 8 B per element
+cross the bus inside the timed kernel.
 `e2e.with_keygen` additionally runs keygen_cmp(32, rng, N) from the host numpy
 Generator (tape drawn on device from its PCG64 state) inside every step.
 
@@ -530,7 +533,8 @@ def run_ours(args, ws, rank, local):
         e2e = {"value": ws * N * args.steps / t_e2e, "unit": "comparisons/s",
                "h2d_bytes_per_step": 2 * N * 8, "d2h_bytes_per_step": 2 * N * 8,
                "step": "fss.eval_cmp(party 0 and 1, HBM-resident keys, pinned host x of 2^%d u64) "
-                       "-> pinned host shares" % args.log2n}
+                       "-> pinned host shares; zero-copy: the kernel loads x from and stores the "
+                       "shares to pinned host memory over PCIe" % args.log2n}
         del k0, k1, alpha, x, y
         torch.cuda.empty_cache()
 

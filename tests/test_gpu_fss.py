@@ -273,9 +273,13 @@ def test_full_size_properties():
     assert torch.equal(rec, (x <= a).to(torch.int64))
 
 
-def test_pinned_host_pipeline_matches_device_path():
-    # pinned host x streams through a 2-stream chunked pipeline (H2D / kernel /
-    # D2H overlap); results must equal the single-launch device path bit-exactly
+def test_host_paths_match_device_path():
+    # pinned host x: the kernel reads x from / writes the shares to pinned host
+    # memory directly (zero-copy); numpy x: staged 2-stream chunked pipeline;
+    # the C-ABI pinned pipeline (fss_dcf_eval_host without staging) too. All
+    # must equal the single-launch device path bit-exactly.
+    import ctypes
+    from paper_2006_04593_b200 import _dev, _lib
     N = (1 << 22) + 12345                 # several chunks plus a ragged tail
     rng = np.random.default_rng(31)
     alpha, k0, k1 = fss.keygen_cmp(32, rng, N)
@@ -292,6 +296,22 @@ def test_pinned_host_pipeline_matches_device_path():
     small = xh[:1000].clone().pin_memory()
     assert torch.equal(fss.eval_cmp(0, k0.take(np.arange(1000)), small).view(torch.int64),
                        fss.eval_cmp(0, k0, xd)[:1000].view(torch.int64).cpu())
+    xn = xh.view(torch.int64).numpy().view(np.uint64)           # pageable numpy copy below
+    got = fss.eval_cmp(1, k1, xn.copy())
+    assert isinstance(got, np.ndarray)
+    assert np.array_equal(got, fss.eval_cmp(1, k1, xd).cpu().view(torch.int64).numpy().view(np.uint64))
+    chunk = 1 << 20
+    out_h = torch.empty(N, dtype=torch.int64, pin_memory=True)
+    scratch = torch.empty((2, 2 * chunk), dtype=torch.uint64, device="cuda")
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    for st in (sa, sb):
+        st.wait_stream(torch.cuda.current_stream())
+    _lib.call("fss_dcf_eval_host", 0, 32, 32, N, N, _dev.ptr(k0.seed0), _dev.ptr(k0.scw), _dev.ptr(k0.tcw),
+              _dev.ptr(k0.sigma_cw), _dev.ptr(k0.leaf_cw), xh.data_ptr(), out_h.data_ptr(),
+              _dev.ptr(scratch[0]), _dev.ptr(scratch[1]), chunk, None, ctypes.c_void_p(sa.cuda_stream),
+              ctypes.c_void_p(sb.cuda_stream))
+    torch.cuda.synchronize()
+    assert torch.equal(out_h, fss.eval_cmp(0, k0, xd).view(torch.int64).cpu())
 
 
 def test_bitsliced_expand_matches_ttable():
