@@ -82,14 +82,15 @@ def to_device_u64(x, device: torch.device) -> torch.Tensor:
             arr = np.array([int(v) & FULL64 for v in arr.reshape(-1)], dtype=np.uint64).reshape(arr.shape)
         else:
             arr = arr.astype(np.int64).astype(np.uint64)
-    arr = np.ascontiguousarray(arr)
+    # np.ascontiguousarray would turn a 0-d array into shape (1,): keep the shape
+    arr = np.require(arr, requirements="C")
     return torch.from_numpy(arr).to(device)
 
 
 def to_device_u8(x, device: torch.device) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         return x.to(device=device, dtype=U8).contiguous()
-    return torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.uint8))).to(device)
+    return torch.from_numpy(np.require(np.asarray(x, dtype=np.uint8), requirements="C")).to(device)
 
 
 def to_numpy(t: torch.Tensor) -> np.ndarray:

@@ -152,3 +152,33 @@ def maxpool_k2(session, x: AdditiveShare, prep: MaxpoolK2Prep) -> AdditiveShare:
                                           _trusted=True), x.precision)
     out = b + relu(session, a - b, prep.level2)
     return out.reshape(*lead, side, side)
+
+
+# ---------------------------------------------------------------------------
+# Preprocessing plans (nn_ops.py:273-292): what the dealer must produce for a
+# layer, derived from shapes alone -- entries ("cmp", count) | ("eq", count) |
+# ("triple", op_tag, geometry), consumed by dealer.preprocess.
+# ---------------------------------------------------------------------------
+
+def relu_plan(m: int) -> list:
+    """ReLU on m elements: m comparison keys + one m-element triple."""
+    from .beaver import ElemwiseGeometry
+    return [("cmp", m), ("triple", "mul", ElemwiseGeometry((m,)))]
+
+
+def argmax_plan(batch: int, m: int) -> list:
+    """Per vector: m*(m-1) comparison keys and m equality keys."""
+    return [("cmp", batch * m * (m - 1)), ("eq", batch * m)]
+
+
+def maxpool_plan(m: int, k: int, stride: int = 2) -> list:
+    from .beaver import ElemwiseGeometry
+    w = ((m - k) // stride + 1) ** 2
+    return argmax_plan(w, k * k) + [("triple", "mul", ElemwiseGeometry((w, k * k)))]
+
+
+def maxpool_k2_plan(m: int) -> list:
+    from .beaver import ElemwiseGeometry
+    w = ((m - 2) // 2 + 1) ** 2
+    return [("cmp", 2 * w), ("triple", "mul", ElemwiseGeometry((w, 2))),
+            ("cmp", w), ("triple", "mul", ElemwiseGeometry((w,)))]
