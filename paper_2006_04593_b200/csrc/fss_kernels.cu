@@ -17,6 +17,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
+#include <omp.h>
 
 #include <type_traits>
 
@@ -708,6 +709,27 @@ int run_host_pipe_pinned(const HostPipe& hp, uint64_t count, Launch launch) {
     return kOk;
 }
 
+// Host memcpy between pageable and pinned memory, split over up to 8 OpenMP
+// threads: one core copies ~4 GB/s on the B200 boxes, so a single-threaded
+// staging copy (2 x 8 B per element) would be slower than the kernel.
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+    constexpr size_t kMin = 1 << 20;
+    int nt = omp_get_max_threads();
+    nt = nt > 8 ? 8 : nt;
+    if (bytes < kMin || nt <= 1) {
+        memcpy(dst, src, bytes);
+        return;
+    }
+    const size_t piece = (bytes / nt + 63) & ~(size_t)63;
+#pragma omp parallel for num_threads(nt) schedule(static)
+    for (int i = 0; i < nt; i++) {
+        const size_t lo = (size_t)i * piece;
+        if (lo < bytes)
+            memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo,
+                   lo + piece <= bytes ? piece : bytes - lo);
+    }
+}
+
 // Pageable host buffers (e.g. numpy arrays): chunks are staged through pinned
 // slots by host memcpy, which overlaps the other slot's copies and kernel.
 // Returns when every share is in out_host.
@@ -726,7 +748,7 @@ int run_host_pipe_staged(const HostPipe& hp, uint64_t count, Launch launch) {
     auto drain = [&](int k) {
         if (!out_busy[k]) return;
         cudaEventSynchronize(d2h[k]);
-        memcpy(hp.out_host + out_lo[k], sout[k], out_m[k] * 8);
+        par_memcpy(hp.out_host + out_lo[k], sout[k], out_m[k] * 8);
         out_busy[k] = false;
     };
     for (uint64_t i = 0, lo = 0; lo < count && rc == kOk; i++, lo += hp.chunk) {
@@ -736,7 +758,7 @@ int run_host_pipe_staged(const HostPipe& hp, uint64_t count, Launch launch) {
         uint64_t* xd = hp.x_dev + slot * hp.chunk;
         uint64_t* od = hp.out_dev + slot * hp.chunk;
         if (in_busy[slot]) cudaEventSynchronize(h2d[slot]);   // staging slot free again
-        memcpy(sin[slot], hp.x_host + lo, m * 8);
+        par_memcpy(sin[slot], hp.x_host + lo, m * 8);
         cudaError_t err = cudaMemcpyAsync(xd, sin[slot], m * 8, cudaMemcpyHostToDevice, s);
         if (err != cudaSuccess) { rc = set_err(kEcuda, "H2D: %s", cudaGetErrorString(err)); break; }
         cudaEventRecord(h2d[slot], s);

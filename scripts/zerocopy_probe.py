@@ -1,8 +1,10 @@
 """Host-buffer evaluation two ways, 2^24 DCF keys (n = 32), party 0 + party 1
 per step, pinned host x in / pinned host shares out:
-  pipeline  -- fss.eval_cmp (chunked H2D / kernel / D2H over two streams);
-  zerocopy  -- the eval kernel reads x from and writes the shares to the pinned
-               host buffers directly (UVA, over PCIe), one launch per party.
+  pipeline  -- fss.eval_cmp on the pinned tensor (since the zero-copy change
+               this IS the zero-copy path; before it, the chunked 2-stream
+               H2D / kernel / D2H pipeline);
+  zerocopy  -- the C ABI called on the host pointers directly;
+  numpy     -- fss.eval_cmp on a pageable numpy array (staged pipeline).
 Wall time per step (median of 5) and bit-equality of the two.
 
   python scripts/zerocopy_probe.py [log2n]
@@ -53,7 +55,14 @@ def timed(fn):
     return sorted(ts)[2]
 
 
-tp, tz = timed(pipeline), timed(zerocopy)
+xn = x.numpy().view(np.uint64).copy()      # pageable numpy input (the reference's calling style)
+
+
+def numpy_path():
+    return fss.eval_cmp(0, k0, xn), fss.eval_cmp(1, k1, xn)
+
+
+tp, tz, tn = timed(pipeline), timed(zerocopy), timed(numpy_path)
 r0, r1 = pipeline()
 z = zerocopy()
 assert torch.equal(r0.view(torch.int64), z[0]) and torch.equal(r1.view(torch.int64), z[1])
@@ -65,4 +74,5 @@ fss.eval_cmp(1, k1, xd)
 b.record()
 b.synchronize()
 print(f"N=2^{log2n}: device-resident {a.elapsed_time(b):.2f} ms, pipeline {tp * 1e3:.2f} ms, "
-      f"zerocopy {tz * 1e3:.2f} ms per step; comparisons/s pipeline {N / tp:.4g}, zerocopy {N / tz:.4g}")
+      f"zerocopy {tz * 1e3:.2f} ms, numpy {tn * 1e3:.2f} ms per step; comparisons/s pinned host "
+      f"{N / tp:.4g} (fss.eval_cmp), zerocopy C-ABI {N / tz:.4g}, numpy (staged pipeline) {N / tn:.4g}")
