@@ -5,9 +5,10 @@
 // in registers. Correction words are stored level-major (struct of arrays,
 // exactly the reference's in-memory layout, fss.py:71-154), so at every level
 // a warp reads 32 consecutive 16-byte scw words (512 B, one coalesced LDG.128
-// per lane) plus 8-byte sigma/leaf words. Grids are persistent: one 512-thread
-// CTA per SM (the 128 KiB T-tables limit residency to one CTA), grid-striding
-// over elements.
+// per lane) plus 8-byte sigma/leaf words. Grids are persistent: one CTA per SM
+// (the 128 KiB T-tables limit residency to one CTA; 1024 threads for eval, 512
+// for keygen), each CTA striding through its own contiguous run of elements
+// (cta_span).
 //
 // Evaluation computes only the AES blocks the output depends on: the block of
 // the child selected by the public input bit (key k1 or k2 chosen per element)
