@@ -16,6 +16,9 @@ stream it in chunks of keys through two pinned host buffers:
   the full key arrays (``fss_arnk_unpack`` with the batch's level stride). A
   party reads only its own payload (half the file).
 
+Each chunk is written / read at its file offset by IO_THREADS threads in
+parallel (os.pwrite / os.preadv release the GIL).
+
 Nothing of the container is ever materialised whole on the host.
 """
 
@@ -29,6 +32,46 @@ from . import _dev, _lib, fss
 from .fss import KIND_CMP, KIND_EQ, KeyFormatError
 
 CHUNK = 1 << 18   # keys per chunk (cmp n = 32: 206 MiB per pinned buffer)
+IO_THREADS = 4    # positional reads / writes of one chunk run in parallel
+_POOL = None
+
+
+def _pool():
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(IO_THREADS, thread_name_prefix="arnk-io")
+    return _POOL
+
+
+def _split(nbytes: int):
+    """Byte ranges of one chunk for the I/O threads (>= 4 MiB each)."""
+    parts = max(1, min(IO_THREADS, nbytes >> 22))
+    step = -(-nbytes // parts)
+    return [(a, min(nbytes, a + step)) for a in range(0, nbytes, step)]
+
+
+def _pwrite_all(fd: int, mv: memoryview, offset: int):
+    """Write mv at file offset with the I/O threads (os.pwrite releases the GIL;
+    one core moves only a few GB/s into the page cache)."""
+    def one(a, b):
+        while a < b:
+            a += os.pwrite(fd, mv[a:b], offset + a)
+    for f in [_pool().submit(one, a, b) for a, b in _split(len(mv))]:
+        f.result()
+
+
+def _pread_all(fd: int, mv: memoryview, offset: int) -> int:
+    def one(a, b):
+        got = 0
+        while a < b:
+            k = os.preadv(fd, [mv[a:b]], offset + a)
+            if k == 0:
+                break
+            a += k
+            got += k
+        return got
+    return sum(f.result() for f in [_pool().submit(one, a, b) for a, b in _split(len(mv))])
 
 
 def _header(kind: int, n: int, count: int) -> bytes:
@@ -79,13 +122,16 @@ def save_keys(path, k0, k1, chunk: int = CHUNK) -> int:
     done = [None, None]
     side = _dev.side_streams(dev, 1)[0]
     written = 0
-    with open(path, "wb") as fh:
-        fh.write(_header(kind, n, count))
+    per = elem * count
+    fd = os.open(path, os.O_WRONLY | os.O_CREAT | os.O_TRUNC, 0o644)
+    try:
+        os.pwrite(fd, _header(kind, n, count), 0)
         written += fss._HEADER_BYTES
-        jobs = [(k, lo, min(count, lo + chunk)) for k in (k0, k1) for lo in range(0, count, chunk)]
+        jobs = [(p, k, lo, min(count, lo + chunk)) for p, k in ((0, k0), (1, k1))
+                for lo in range(0, count, chunk)]
 
         def issue(i):
-            k, lo, hi = jobs[i]
+            _, k, lo, hi = jobs[i]
             b = i & 1
             side.wait_stream(torch.cuda.current_stream(dev))
             with torch.cuda.stream(side):
@@ -104,8 +150,11 @@ def save_keys(path, k0, k1, chunk: int = CHUNK) -> int:
             if i + 1 < len(jobs):
                 issue(i + 1)          # packs into the other pinned buffer meanwhile
             ev.synchronize()
-            fh.write(memoryview(pinned[b].numpy())[:nbytes])
+            p, _, lo, _ = jobs[i]
+            _pwrite_all(fd, memoryview(pinned[b].numpy())[:nbytes], fss._HEADER_BYTES + p * per + lo * elem)
             written += nbytes
+    finally:
+        os.close(fd)
     return written
 
 
@@ -142,14 +191,13 @@ def load_keys(path, party: int = None, device=None, chunk: int = CHUNK):
         stream = torch.cuda.current_stream(dev)
         for p in parties:
             k = keys[p]
-            fh.seek(fss._HEADER_BYTES + p * per)
             for i, lo in enumerate(range(0, count, chunk)):
                 hi = min(count, lo + chunk)
                 b = i & 1
                 if used[b] is not None:
                     used[b].synchronize()      # the copy that last read this pinned buffer is done
                 view = memoryview(pinned[b].numpy())[: (hi - lo) * elem]
-                got = fh.readinto(view)
+                got = _pread_all(fh.fileno(), view, fss._HEADER_BYTES + p * per + lo * elem)
                 if got != (hi - lo) * elem:
                     raise KeyFormatError("truncated payload")
                 dst = staged[b][: (hi - lo) * elem]
