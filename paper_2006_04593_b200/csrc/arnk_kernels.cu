@@ -274,8 +274,8 @@ constexpr int kBatch = FSSB_ARNK_BATCH;   // row loads in flight per thread (pac
 // whose byte range is not 16-byte aligned (only the last, partial tile can be)
 // falls back to a cooperative copy. KIND and the ring width W are template
 // parameters so every record layout is compile-time.
-template <bool PACK, int KIND, int W>
-__global__ void __launch_bounds__(kArnkThreads)
+template <bool PACK, int KIND, int W, int THREADS = kArnkThreads>
+__global__ void __launch_bounds__(THREADS)
 arnk_tile_kernel(int n, uint64_t count, uint64_t ld, int lnb, uint32_t stride, int use_tma, Keys k,
                  uint8_t* buf) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -338,14 +338,14 @@ arnk_tile_kernel(int n, uint64_t count, uint64_t ld, int lnb, uint32_t stride, i
         // per-level records (scw | flags | sigma)
         const uint32_t items = pair_items((uint32_t)n, lnb, d_lv);
         if (PACK) {
-            for (uint32_t base = threadIdx.x; base < items; base += kBatch * kArnkThreads) {
+            for (uint32_t base = threadIdx.x; base < items; base += kBatch * THREADS) {
                 uint4 v[kBatch];
                 uint32_t f[kBatch], so[kBatch];
                 uint64_t sg[kBatch];
                 bool ok[kBatch];
 #pragma unroll
                 for (int u = 0; u < kBatch; u++) {   // all loads first: kBatch rows in flight
-                    const uint32_t idx = base + u * kArnkThreads;
+                    const uint32_t idx = base + u * THREADS;
                     const Item it = pair_item(idx, lnb, d_lv);
                     ok[u] = idx < items && it.row < (uint32_t)n && it.e < m;
                     if (ok[u]) {
@@ -365,7 +365,7 @@ arnk_tile_kernel(int n, uint64_t count, uint64_t ld, int lnb, uint32_t stride, i
                 }
             }
         } else {
-            for (uint32_t idx = threadIdx.x; idx < items; idx += kArnkThreads) {
+            for (uint32_t idx = threadIdx.x; idx < items; idx += THREADS) {
                 const Item it = pair_item(idx, lnb, d_lv);
                 if (it.row >= (uint32_t)n || it.e >= m) continue;
                 const uint64_t off = (uint64_t)it.row * ld + e0 + it.e;
@@ -376,7 +376,7 @@ arnk_tile_kernel(int n, uint64_t count, uint64_t ld, int lnb, uint32_t stride, i
             }
         }
         // element head (alpha share, seed) and the eq tail (cw_final)
-        for (uint32_t e = threadIdx.x; e < m; e += kArnkThreads) {
+        for (uint32_t e = threadIdx.x; e < m; e += THREADS) {
             const uint32_t so = e * EB;
             if (PACK) {
                 sput_u64<W>(tile, so, k.alpha_share[e0 + e]);
@@ -392,13 +392,13 @@ arnk_tile_kernel(int n, uint64_t count, uint64_t ld, int lnb, uint32_t stride, i
         if (KIND == 1) {
             const uint32_t leaf_items = pair_items((uint32_t)n + 1, lnb, d_leaf);
             if (PACK) {
-                for (uint32_t base = threadIdx.x; base < leaf_items; base += kBatch * kArnkThreads) {
+                for (uint32_t base = threadIdx.x; base < leaf_items; base += kBatch * THREADS) {
                     uint64_t v[kBatch];
                     uint32_t so[kBatch];
                     bool ok[kBatch];
 #pragma unroll
                     for (int u = 0; u < kBatch; u++) {
-                        const uint32_t idx = base + u * kArnkThreads;
+                        const uint32_t idx = base + u * THREADS;
                         const Item it = pair_item(idx, lnb, d_leaf);
                         ok[u] = idx < leaf_items && it.row <= (uint32_t)n && it.e < m;
                         if (ok[u]) {
@@ -411,7 +411,7 @@ arnk_tile_kernel(int n, uint64_t count, uint64_t ld, int lnb, uint32_t stride, i
                         if (ok[u]) sput_u64<W>(tile, so[u], v[u]);
                 }
             } else {
-                for (uint32_t idx = threadIdx.x; idx < leaf_items; idx += kArnkThreads) {
+                for (uint32_t idx = threadIdx.x; idx < leaf_items; idx += THREADS) {
                     const Item it = pair_item(idx, lnb, d_leaf);
                     if (it.row > (uint32_t)n || it.e >= m) continue;
                     k.leaf_cw[(uint64_t)it.row * ld + e0 + it.e] = sget<W>(tile, it.e * EB + tail + it.row * W);
@@ -614,6 +614,9 @@ int arnk_tile_lnb(bool pack, int kind, int n) {
     return 2 * elem_bytes(kind, n) * 64 <= kb * 1024 ? 2 : 1;
 }
 
+#ifndef FSSB_ARNK_UNPACK_THREADS
+#define FSSB_ARNK_UNPACK_THREADS 256
+#endif
 #ifndef FSSB_ARNK_ASYNC_PACK
 #define FSSB_ARNK_ASYNC_PACK 1
 #endif
@@ -663,18 +666,19 @@ cudaError_t launch_tile(int n, uint64_t count, uint64_t ld, Keys k, uint8_t* buf
     const uint32_t stride = (uint32_t)((elem_bytes(KIND, n) * E + 16 + 127) / 128 * 128);
     const size_t smem = 128 + 2 * (size_t)stride;
     int dev = 0, sms = 0, per_sm = 1;
-    auto kern = arnk_tile_kernel<PACK, KIND, W>;
+    constexpr int kThr = PACK ? kArnkThreads : FSSB_ARNK_UNPACK_THREADS;
+    auto kern = arnk_tile_kernel<PACK, KIND, W, kThr>;
     cudaError_t err = cudaGetDevice(&dev);
     if (err == cudaSuccess) err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (err == cudaSuccess) err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err == cudaSuccess) err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kArnkThreads, smem);
+    if (err == cudaSuccess) err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThr, smem);
     if (err != cudaSuccess) return err;
     const uint64_t tiles = (count + E - 1) / E;
     const uint64_t cap = (uint64_t)sms * (per_sm > 0 ? per_sm : 1);
     // FSSB_ARNK_NO_TMA=1 (environment): cooperative copies instead of the bulk
     // engine -- for compute-sanitizer initcheck, which does not see TMA writes
     static const int use_tma = getenv("FSSB_ARNK_NO_TMA") ? 0 : 1;
-    kern<<<(unsigned)(tiles < cap ? tiles : cap), kArnkThreads, smem, st>>>(n, count, ld, lnb, stride, use_tma,
+    kern<<<(unsigned)(tiles < cap ? tiles : cap), kThr, smem, st>>>(n, count, ld, lnb, stride, use_tma,
                                                                            k, buf);
     return cudaGetLastError();
 }

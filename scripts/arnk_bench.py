@@ -24,7 +24,8 @@ VDIR = os.path.join(ROOT, "build", "variants")
 # variant name -> compile-time defines (the shipped library is "main")
 VARIANTS = {
     "naive": ["FSSB_ARNK_NAIVE=1"],
-    "sync_pack": ["FSSB_ARNK_ASYNC_PACK=0"],
+    "unpack512": ["FSSB_ARNK_UNPACK_THREADS=512"],
+    "unpack512_e32": ["FSSB_ARNK_UNPACK_THREADS=512", "FSSB_ARNK_UNPACK_TILE_KB=100"],
 }
 
 
