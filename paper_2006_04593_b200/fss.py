@@ -561,9 +561,11 @@ def _run_eval(launch, xt, host, count: int, dev, host_launch=None, out=None):
 def _prep_x(x, count: int, n: int, dev):
     """_broadcast_x plus the host fast paths (no upload here; the kernels reduce
     x mod 2^n themselves)."""
-    if isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned() and x.numel() == count \
-            and x.dtype in (torch.uint64, torch.int64):
-        return x.reshape(-1).contiguous(), "torch_pinned"
+    if isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned() and x.is_contiguous() \
+            and x.numel() == count and x.dtype in (torch.uint64, torch.int64):
+        # contiguous pinned memory only: the zero-copy kernel reads it in place
+        # (a non-contiguous view would be copied into pageable memory first)
+        return x.reshape(-1), "torch_pinned"
     if isinstance(x, np.ndarray) and x.size == count and count >= PIPELINE_MIN \
             and x.dtype in (np.uint64, np.int64):
         return np.ascontiguousarray(x.reshape(-1)).view(np.uint64), "numpy"

@@ -393,3 +393,17 @@ def test_numpy_host_pipeline_matches_device_path():
     assert np.array_equal(fss.eval_eq(0, e0, x), _np(fss.eval_eq(0, e0, xd)))
     yl, lv = fss.eval_cmp(0, k0, x, return_levels=True)
     assert np.array_equal(yl, y) and lv.shape == (33, N)
+
+
+def test_pinned_noncontiguous_input_is_uploaded_not_read_in_place():
+    # a strided view of pinned memory is not itself readable in place: it must
+    # take the upload path (and still give the device path's shares)
+    N = 4096
+    _, k0, _ = fss.keygen_cmp(32, np.random.default_rng(5), N)
+    big = torch.from_numpy(np.random.default_rng(6).integers(0, 1 << 32, 2 * N, dtype=np.uint64)
+                           .view(np.int64)).pin_memory()
+    xv = big[::2]
+    assert xv.is_pinned() and not xv.is_contiguous()
+    got = fss.eval_cmp(0, k0, xv)
+    want = fss.eval_cmp(0, k0, xv.contiguous().cuda())
+    assert torch.equal(torch.as_tensor(got).view(torch.int64).cpu().reshape(-1), want.view(torch.int64).cpu())
