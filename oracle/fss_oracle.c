@@ -10,7 +10,10 @@
  * Parity of this restatement is pinned (tests/test_oracle.py) against
  *   - the reference's 15 committed PRG vectors (pkg/prg_vectors.txt:3-17), and
  *   - golden fixtures produced by running the Python reference itself in the
- *     build container (tests/golden/make_golden.py, fixtures in tests/golden).
+ *     build container (tests/golden/make_golden.py, fixtures in tests/golden),
+ *   - sha256 digests of the reference's keys / shares at the BASELINE sizes
+ *     (DCF 2^16, DPF 2^20: tests/golden/make_large_golden.py,
+ *     tests/test_large_golden.py).
  *
  * Algorithms follow the reference line by line, including its over-computation
  * (eval expands 2 / 3 blocks per level exactly as fss.py:365 / fss.py:395 do), so
