@@ -154,6 +154,18 @@ int fss_dpf_eval_host(int party, int n, uint64_t count, uint64_t ld, const uint8
                       const uint64_t* x_host, uint64_t* out_host, uint64_t* x_dev, uint64_t* out_dev,
                       uint64_t chunk, uint64_t* stage, void* stream_a, void* stream_b);
 
+/* eval_cmp / eval_eq straight from one party's ARNK payload rows (the
+ * element-major container layout, LAYOUT.md:48-71; payload = count *
+ * fss_arnk_elem_bytes(kind, n) bytes, as fss_arnk_pack writes them) instead of
+ * unpacked level-major keys: a party that loads a key file evaluates without
+ * the unpack pass. out_bits == n (packed keys carry one width). Public input:
+ * x, or (x == NULL) the opening of the two wire-packed masked messages as in
+ * fss_*_eval_masked. New (no reference counterpart). */
+int fss_dcf_eval_packed(int party, int n, uint64_t count, const uint8_t* payload, const uint64_t* x,
+                        const void* m_own, const void* m_peer, uint64_t* out, void* stream);
+int fss_dpf_eval_packed(int party, int n, uint64_t count, const uint8_t* payload, const uint64_t* x,
+                        const void* m_own, const void* m_peer, uint64_t* out, void* stream);
+
 /* ARNK per-party payloads (LAYOUT.md:48-71; fss._pack_eq/_pack_cmp fss.py:540-583,
  * _unpack_eq/_unpack_cmp fss.py:553-602). kind 0 = equality, 1 = comparison.
  * payload is count * fss_arnk_elem_bytes(kind, n) bytes, element-major.

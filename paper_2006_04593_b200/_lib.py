@@ -55,6 +55,8 @@ SIGNATURES = {
     "fss_dcf_eval_masked": [_int, _int, _int, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "fss_dcf_eval_host": [_int, _int, _int, _u64, _u64] + [_vp] * 9 + [_u64, _vp, _vp, _vp],
     "fss_dpf_eval_host": [_int, _int, _u64, _u64] + [_vp] * 8 + [_u64, _vp, _vp, _vp],
+    "fss_dcf_eval_packed": [_int, _int, _u64, _vp, _vp, _vp, _vp, _vp, _vp],
+    "fss_dpf_eval_packed": [_int, _int, _u64, _vp, _vp, _vp, _vp, _vp, _vp],
     "fss_arnk_elem_bytes": [_int, _int],
     "fss_arnk_pack": [_int, _int, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "fss_arnk_unpack": [_int, _int, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],

@@ -287,6 +287,135 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
     }
 }
 
+// ------------------------------------------------ eval from ARNK payloads
+// A party that receives its keys as an ARNK container (reference cli.py:150-160:
+// read the file, unpack, evaluate once -- the keys are single-use) can
+// evaluate straight from the element-major payload rows, skipping the unpack
+// pass (fss_arnk_unpack) and the level-major copy entirely. Element e's record
+// (LAYOUT.md:48-71) is read front to back by its own thread, one level record
+// (scw 16 | flags 1 | sigma w) per level: lanes hit different lines, but each
+// thread streams its own 824-byte record sequentially, so the L1 (what the
+// T-tables leave of it) serves the rest of each sector and DRAM traffic stays
+// at the payload bytes. Records sit at odd byte offsets: they are read as
+// aligned 32-bit words and realigned with funnel shifts.
+
+// The NB bytes at p (any alignment) as little-endian words o[0..(NB+3)/4):
+// exactly the aligned 32-bit words that hold those bytes are loaded (so the
+// last record of the last element never reads past the payload), then
+// realigned with funnel shifts; bytes of o beyond NB are unspecified.
+template <int NB>
+__device__ __forceinline__ void ld_stream(const uint8_t* p, uint32_t (&o)[(NB + 3) / 4]) {
+    constexpr int NO = (NB + 3) / 4, NWMAX = (NB + 6) / 4;   // output words, words touched at worst
+    const uint32_t* a = reinterpret_cast<const uint32_t*>((uintptr_t)p & ~(uintptr_t)3);
+    const uint32_t off = (uint32_t)(uintptr_t)p & 3u;
+    const uint32_t last = (off + NB - 1) >> 2;             // last word holding a wanted byte
+    uint32_t w[NWMAX + 1];
+#pragma unroll
+    for (int j = 0; j < NWMAX; j++) w[j] = (uint32_t)j <= last ? __ldg(a + j) : 0u;
+    w[NWMAX] = 0u;
+#pragma unroll
+    for (int j = 0; j < NO; j++) o[j] = __funnelshift_r(w[j], w[j + 1], 8 * off);
+}
+
+// A W-byte little-endian ring value at p.
+template <int W>
+__device__ __forceinline__ uint64_t ld_ring(const uint8_t* p) {
+    uint32_t o[(W + 3) / 4];
+    ld_stream<W>(p, o);
+    uint64_t v = o[0];
+    if (W > 4) v |= (uint64_t)o[(W + 3) / 4 - 1] << 32;
+    return W >= 8 ? v : v & ((1ULL << (8 * W)) - 1);
+}
+
+template <int W>
+__global__ void __launch_bounds__(kThreads, 1)
+dcf_eval_packed_kernel(int party, int n, uint64_t count, const uint8_t* __restrict__ payload,
+                       const uint64_t* __restrict__ x, const void* __restrict__ m_own,
+                       const void* __restrict__ m_peer, uint64_t* __restrict__ out) {
+    extern __shared__ uint32_t tab[];
+    fssb::fill_tables(tab);
+    __syncthreads();
+    const fssb::Tab tb = fssb::make_tab(tab);
+    constexpr uint32_t rec = 17 + W;
+    constexpr int NW = (17 + W + 3) / 4;          // words of one level record
+    const uint64_t EB = W + 16 + (uint64_t)n * rec + (uint64_t)(n + 1) * W;
+    const uint32_t tail = W + 16 + n * rec;       // the leaf block
+    const uint64_t mask = ring_mask(n);           // packed keys: out_bits == n
+    const Span sp = cta_span(count);
+    for (uint64_t e = sp.lo + threadIdx.x; e < sp.hi; e += blockDim.x) {
+        const uint8_t* kp = payload + e * EB;
+        uint32_t sw[4];
+        ld_stream<16>(kp + W, sw);
+        U4 s = U4{sw[0], sw[1], sw[2], sw[3]};
+        uint32_t t = party;
+        uint64_t acc = 0;
+        const uint64_t xe = load_x(x, m_own, m_peer, n, e) & mask;
+        for (int i = 0; i < n; i++) {
+            uint32_t o[NW];
+            ld_stream<rec>(kp + W + 16 + (uint32_t)i * rec, o);
+            const U4 cw = U4{o[0], o[1], o[2], o[3]};
+            const uint32_t f = o[4] & 0xFFu;
+            uint64_t sig = (uint64_t)__funnelshift_r(o[4], NW > 5 ? o[5] : 0u, 8);
+            if (W > 3) sig |= (uint64_t)__funnelshift_r(NW > 5 ? o[5] : 0u, NW > 6 ? o[6] : 0u, 8) << 32;
+            if (W < 8) sig &= (1ULL << (8 * W)) - 1;
+            const uint64_t leaf = ld_ring<W>(kp + tail + (uint32_t)i * W);
+            const uint32_t xb = (uint32_t)(xe >> (n - 1 - i)) & 1u;
+            const U4 a = fssb::mmo<0, true>(tb, s, 0u - xb);
+            const uint32_t tm = 0u - t;
+            uint32_t lane_lo, lane_hi;
+            fssb::mmo_half<2>(tb, s, 0u - xb, lane_lo, lane_hi);
+            const uint64_t lane = ((uint64_t)lane_hi << 32) | lane_lo;
+            const uint32_t tau = ((lane_hi >> 31) ^ (t & (f >> (2 + xb)))) & 1u;
+            const uint64_t sigma = lane ^ (sig & (0 - (uint64_t)t));
+            acc += (leaf & (0 - (uint64_t)tau)) + sigma;
+            s = xor4(a, and4(cw, tm));
+            const uint32_t tn = ((a.w >> 31) ^ (t & (f >> xb))) & 1u;
+            s.w &= 0x7FFFFFFFu;
+            t = tn;
+        }
+        acc += (ld_ring<W>(kp + tail + (uint32_t)n * W) & (0 - (uint64_t)t)) + lo64(s);
+        out[e] = (party ? (0 - acc) : acc) & mask;
+    }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kThreads, 1)
+dpf_eval_packed_kernel(int party, int n, uint64_t count, const uint8_t* __restrict__ payload,
+                       const uint64_t* __restrict__ x, const void* __restrict__ m_own,
+                       const void* __restrict__ m_peer, uint64_t* __restrict__ out) {
+    extern __shared__ uint32_t tab[];
+    fssb::fill_tables(tab);
+    __syncthreads();
+    const fssb::Tab tb = fssb::make_tab(tab);
+    const uint64_t EB = W + 16 + 17 * (uint64_t)n + W;
+    const uint64_t mask = ring_mask(n);
+    const Span sp = cta_span(count);
+    for (uint64_t e = sp.lo + threadIdx.x; e < sp.hi; e += blockDim.x) {
+        const uint8_t* kp = payload + e * EB;
+        uint32_t sw[4];
+        ld_stream<16>(kp + W, sw);
+        U4 s = U4{sw[0], sw[1], sw[2], sw[3]};
+        uint32_t t = party;
+        const uint64_t xe = load_x(x, m_own, m_peer, n, e) & mask;
+        for (int i = 0; i < n; i++) {
+            uint32_t o[5];
+            ld_stream<17>(kp + W + 16 + 17u * i, o);
+            const U4 cw = U4{o[0], o[1], o[2], o[3]};
+            const uint32_t f = o[4] & 0xFFu;
+            const uint32_t xb = (uint32_t)(xe >> (n - 1 - i)) & 1u;
+            const U4 a = fssb::mmo<0, true>(tb, s, 0u - xb);
+            s = xor4(a, and4(cw, 0u - t));
+            const uint32_t tn = ((a.w >> 31) ^ (t & (f >> xb))) & 1u;
+            s.w &= 0x7FFFFFFFu;
+            t = tn;
+        }
+        const uint64_t cwf = ld_ring<W>(kp + W + 16 + 17u * n);
+        uint64_t o = (((uint64_t)t * cwf) + lo64(s)) & mask;
+        if (party) o = (0 - o) & mask;
+        out[e] = o;
+    }
+}
+
 // -------------------------------------------------------------- DPF keygen
 // fss._keygen_eq_core (fss.py:173-216): both parties' walks, 4 AES blocks/level.
 __global__ void __launch_bounds__(kKeygenThreads, 1)
@@ -854,6 +983,58 @@ int fss_dcf_eval_masked(int party, int n, int out_bits, uint64_t count, uint64_t
                         const void* m_peer, uint64_t* out, void* stream) {
     return launch_dcf_eval(party, n, out_bits, count, ld, seed0, scw, tcw, sigma_cw, leaf_cw, nullptr,
                            m_own, m_peer, out, nullptr, stream);
+}
+
+int fss_dcf_eval_packed(int party, int n, uint64_t count, const uint8_t* payload, const uint64_t* x,
+                        const void* m_own, const void* m_peer, uint64_t* out, void* stream) {
+    if (party != 0 && party != 1) return set_err(kEinval, "party must be 0 or 1%s");
+    if (n < 1 || n > 63) return set_err(kEinval, "n out of range%s");
+    if (count == 0) return kOk;
+    if (!x && (!m_own || !m_peer)) return set_err(kEinval, "need x or both masked messages%s");
+    void (*kern)(int, int, uint64_t, const uint8_t*, const uint64_t*, const void*, const void*, uint64_t*);
+    switch ((n + 7) / 8) {
+        case 1: kern = dcf_eval_packed_kernel<1>; break;
+        case 2: kern = dcf_eval_packed_kernel<2>; break;
+        case 3: kern = dcf_eval_packed_kernel<3>; break;
+        case 4: kern = dcf_eval_packed_kernel<4>; break;
+        case 5: kern = dcf_eval_packed_kernel<5>; break;
+        case 6: kern = dcf_eval_packed_kernel<6>; break;
+        case 7: kern = dcf_eval_packed_kernel<7>; break;
+        default: kern = dcf_eval_packed_kernel<8>; break;
+    }
+    int sms;
+    if (int rc = prep_launch(kern, &sms)) return rc;
+    int threads;
+    const int grid = eval_grid(count, sms, &threads);
+    kern<<<grid, threads, fssb::kTableBytes, (cudaStream_t)stream>>>(party, n, count, payload, x, m_own, m_peer,
+                                                                      out);
+    return check_launch();
+}
+
+int fss_dpf_eval_packed(int party, int n, uint64_t count, const uint8_t* payload, const uint64_t* x,
+                        const void* m_own, const void* m_peer, uint64_t* out, void* stream) {
+    if (party != 0 && party != 1) return set_err(kEinval, "party must be 0 or 1%s");
+    if (n < 1 || n > 64) return set_err(kEinval, "n out of range%s");
+    if (count == 0) return kOk;
+    if (!x && (!m_own || !m_peer)) return set_err(kEinval, "need x or both masked messages%s");
+    void (*kern)(int, int, uint64_t, const uint8_t*, const uint64_t*, const void*, const void*, uint64_t*);
+    switch ((n + 7) / 8) {
+        case 1: kern = dpf_eval_packed_kernel<1>; break;
+        case 2: kern = dpf_eval_packed_kernel<2>; break;
+        case 3: kern = dpf_eval_packed_kernel<3>; break;
+        case 4: kern = dpf_eval_packed_kernel<4>; break;
+        case 5: kern = dpf_eval_packed_kernel<5>; break;
+        case 6: kern = dpf_eval_packed_kernel<6>; break;
+        case 7: kern = dpf_eval_packed_kernel<7>; break;
+        default: kern = dpf_eval_packed_kernel<8>; break;
+    }
+    int sms;
+    if (int rc = prep_launch(kern, &sms)) return rc;
+    int threads;
+    const int grid = eval_grid(count, sms, &threads);
+    kern<<<grid, threads, fssb::kTableBytes, (cudaStream_t)stream>>>(party, n, count, payload, x, m_own, m_peer,
+                                                                      out);
+    return check_launch();
 }
 
 int fss_dpf_keygen(int n, uint64_t count, const uint64_t* alpha, const uint64_t* alpha0,

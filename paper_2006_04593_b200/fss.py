@@ -207,6 +207,97 @@ class CmpKeyBatch:
         return _take_unused(self, m)
 
 
+@dataclass
+class PackedKeyBatch:
+    """One party's keys kept as their ARNK payload rows (count, elem) u8 on the
+    device -- the element-major container layout of ``_pack_eq`` /
+    ``_pack_cmp`` (fss.py:540-583, LAYOUT.md:48-71) -- instead of the
+    level-major arrays. ``eval_eq`` / ``eval_cmp`` / ``sign_protocol`` /
+    ``eq_protocol`` accept it and evaluate straight from the rows
+    (fss_*_eval_packed), so a party that loads a key file
+    (``keyfile.load_keys(..., packed=True)``) skips the unpack pass. New (no
+    reference counterpart); ``unpack()`` gives the reference's typed batch."""
+
+    kind: int                  # KIND_EQ / KIND_CMP
+    party: int
+    n_bits: int
+    payload: torch.Tensor      # (count, elem_bytes) u8, device
+    consumed: np.ndarray = field(default=None)
+
+    def __post_init__(self):
+        if self.consumed is None:
+            self.consumed = np.zeros(self.count, dtype=bool)
+
+    @property
+    def count(self) -> int:
+        return int(self.payload.shape[0])
+
+    @property
+    def device(self):
+        return self.payload.device
+
+    @property
+    def out_bits(self) -> int:
+        return self.n_bits              # a container carries one ring width
+
+    @property
+    def alpha_share(self) -> torch.Tensor:
+        """The w-byte little-endian alpha share at the front of every row."""
+        w = _ring_width_bytes(self.n_bits)
+        b = self.payload[:, :w].to(torch.int64)
+        v = torch.zeros(self.count, dtype=torch.int64, device=self.device)
+        for i in range(w):
+            v |= b[:, i] << (8 * i)
+        return v.view(torch.uint64)
+
+    def validate(self):
+        elem = eq_elem_bytes(self.n_bits) if self.kind == KIND_EQ else cmp_elem_bytes(self.n_bits)
+        if self.kind not in (KIND_EQ, KIND_CMP):
+            raise KeyFormatError(f"unknown key kind {self.kind}")
+        if not isinstance(self.payload, torch.Tensor) or not self.payload.is_cuda:
+            raise KeyFormatError("payload must be a device tensor")
+        if self.payload.dtype != torch.uint8 or self.payload.ndim != 2 or self.payload.shape[1] != elem:
+            raise KeyFormatError(f"payload must be (count, {elem}) uint8")
+        if not self.payload.is_contiguous():
+            raise KeyFormatError("payload rows must be contiguous")
+
+    def take(self, idx) -> "PackedKeyBatch":
+        sel, arr = _index(idx, self.count, self.device)
+        return PackedKeyBatch(self.kind, self.party, self.n_bits, _take1(self.payload, sel),
+                              self.consumed[arr].copy())
+
+    def take_unused(self, m: int) -> "PackedKeyBatch":
+        return _take_unused(self, m)
+
+    def unpack(self):
+        """The reference's typed batch (EqKeyBatch / CmpKeyBatch)."""
+        self.validate()
+        k = _unpack(self.kind, self.party, self.n_bits, self.count, self.payload.reshape(-1), self.device)
+        k.consumed = self.consumed.copy()
+        return k
+
+
+def _eval_packed(party: int, k: PackedKeyBatch, x, out, m_own=None, m_peer=None):
+    """Evaluation straight from payload rows (fss_dcf/dpf_eval_packed)."""
+    k.validate()
+    fn = "fss_dcf_eval_packed" if k.kind == KIND_CMP else "fss_dpf_eval_packed"
+    n, count, dev = k.n_bits, k.count, k.device
+    if m_own is not None:          # the masked round's opening happens in the kernel
+        res = torch.empty(count, dtype=torch.uint64, device=dev)
+        with torch.cuda.device(dev):
+            _lib.call(fn, int(party), n, count, _dev.ptr(k.payload), None, _dev.ptr(m_own),
+                      _dev.ptr(m_peer), _dev.ptr(res), _dev.stream_handle(dev))
+        return res
+    out = _check_out(out, count, dev)
+    xt, host = _prep_x(x, count, n, dev)
+
+    def launch(lo, hi, xd, od, stream):
+        with torch.cuda.device(dev):
+            _lib.call(fn, int(party), n, hi - lo, _dev.ptr(k.payload[lo:hi]), _dev.ptr(xd), None, None,
+                      _dev.ptr(od), stream)
+    return _run_eval(launch, xt, host, count, dev, None, out)
+
+
 def _take_unused(batch, m: int):
     """Single-use key hand-out (fss.py:157-166): the first m unconsumed keys.
 
@@ -574,7 +665,9 @@ def _prep_x(x, count: int, n: int, dev):
 
 def eval_eq(party: int, k: EqKeyBatch, x, out=None):
     """Per-party share of 1[x == alpha] (fss.py:357-377) via fss_dpf_eval.
-    ``out``: as for eval_cmp."""
+    ``out``: as for eval_cmp. ``k`` may be a PackedKeyBatch."""
+    if isinstance(k, PackedKeyBatch):
+        return _eval_packed(party, k, x, out)
     k.validate()
     n, count, dev = k.n_bits, k.count, k.device
     out = _check_out(out, count, dev)
@@ -603,7 +696,12 @@ def eval_cmp(party: int, k: CmpKeyBatch, x, return_levels: bool = False, out=Non
     shape (n+1, count); at most one level reconstructs to 1. ``out`` (device
     input only, extension): write the shares into this device buffer of count
     u64 words -- e.g. a slot of another GPU's gather buffer (shard.PeerGather),
-    so the kernel's stores are the output collective."""
+    so the kernel's stores are the output collective. ``k`` may be a
+    PackedKeyBatch (evaluated straight from its ARNK rows)."""
+    if isinstance(k, PackedKeyBatch):
+        if return_levels:
+            return eval_cmp(party, k.unpack(), x, return_levels=True)
+        return _eval_packed(party, k, x, out)
     k.validate()
     n, count, dev = k.n_bits, k.count, k.device
     out = _check_out(out, count, dev)
@@ -668,6 +766,8 @@ def _masked_round(session, y, alpha_share, n: int, op: str):
 
 
 def _eval_cmp_masked(party: int, k: CmpKeyBatch, m_own, m_peer) -> torch.Tensor:
+    if isinstance(k, PackedKeyBatch):
+        return _eval_packed(party, k, None, None, m_own, m_peer)
     k.validate()
     dev = k.device
     ld = _eval_operands(k, ("tcw", "sigma_cw", "leaf_cw"))
@@ -682,6 +782,8 @@ def _eval_cmp_masked(party: int, k: CmpKeyBatch, m_own, m_peer) -> torch.Tensor:
 
 
 def _eval_eq_masked(party: int, k: EqKeyBatch, m_own, m_peer) -> torch.Tensor:
+    if isinstance(k, PackedKeyBatch):
+        return _eval_packed(party, k, None, None, m_own, m_peer)
     k.validate()
     dev = k.device
     ld = _eval_operands(k, ("tcw",))

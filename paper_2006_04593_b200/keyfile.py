@@ -171,10 +171,12 @@ def _alloc(kind: int, party: int, n: int, count: int, dev):
     return fss.CmpKeyBatch(party, n, alpha, seed0, scw, tcw, sigma, leaf)
 
 
-def load_keys(path, party: int = None, device=None, chunk: int = CHUNK):
+def load_keys(path, party: int = None, device=None, chunk: int = CHUNK, packed: bool = False):
     """Read an ARNK key file into HBM. ``party`` None -> (k0, k1) as
     ``unpack_keys(deserialize_keys(data))``; 0 or 1 -> that party's batch only
-    (only its payload is read)."""
+    (only its payload is read). ``packed=True``: keep the payload rows as they
+    are (fss.PackedKeyBatch, evaluated straight from the rows) -- no unpack
+    pass, and 824 instead of 1,088 bytes of HBM per DCF key at n = 32."""
     if party not in (None, 0, 1):
         raise ValueError("party must be 0, 1 or None")
     size = os.path.getsize(path)
@@ -183,10 +185,14 @@ def load_keys(path, party: int = None, device=None, chunk: int = CHUNK):
         dev = _dev.default_device(device)
         elem = _elem(kind, n)
         parties = (0, 1) if party is None else (party,)
-        keys = {p: _alloc(kind, p, n, count, dev) for p in parties}
+        if packed:
+            keys = {p: fss.PackedKeyBatch(kind, p, n, torch.empty((count, elem), dtype=torch.uint8,
+                                                                  device=dev)) for p in parties}
+        else:
+            keys = {p: _alloc(kind, p, n, count, dev) for p in parties}
         chunk = max(1, min(chunk, max(count, 1)))
         pinned = [torch.empty(chunk * elem, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
-        staged = [torch.empty(chunk * elem, dtype=torch.uint8, device=dev) for _ in range(2)]
+        staged = [] if packed else [torch.empty(chunk * elem, dtype=torch.uint8, device=dev) for _ in range(2)]
         used = [None, None]
         stream = torch.cuda.current_stream(dev)
         for p in parties:
@@ -200,6 +206,12 @@ def load_keys(path, party: int = None, device=None, chunk: int = CHUNK):
                 got = _pread_all(fh.fileno(), view, fss._HEADER_BYTES + p * per + lo * elem)
                 if got != (hi - lo) * elem:
                     raise KeyFormatError("truncated payload")
+                if packed:                     # rows land in place: no unpack
+                    k.payload[lo:hi].view(-1).copy_(pinned[b][: (hi - lo) * elem], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(stream)
+                    used[b] = ev
+                    continue
                 dst = staged[b][: (hi - lo) * elem]
                 dst.copy_(pinned[b][: (hi - lo) * elem], non_blocking=True)
                 with torch.cuda.device(dev):

@@ -98,3 +98,48 @@ def test_pack_of_column_views_matches_full_payload(kind, n, count):
                            got.reshape(-1), DEV)
         _same(back, k0.take(np.arange(lo, hi)))
     assert elem == (fss.cmp_elem_bytes(n) if kind == "cmp" else fss.eq_elem_bytes(n))
+
+
+@pytest.mark.parametrize("kind,n,count", [("cmp", 32, 3001), ("cmp", 8, 100), ("cmp", 12, 257),
+                                          ("cmp", 63, 50), ("eq", 32, 2000), ("eq", 5, 77),
+                                          ("eq", 64, 40), ("eq", 16, 1)])
+def test_packed_keys_evaluate_like_unpacked(tmp_path, kind, n, count):
+    """Keys loaded packed (payload rows kept, fss_*_eval_packed) give the same
+    shares as the unpacked keys -- eval with x, and the masked sign / eq
+    protocols -- and take / take_unused / unpack behave like the typed batch."""
+    from paper_2006_04593_b200 import runtime
+    from paper_2006_04593_b200.ring import RingTensor
+    from paper_2006_04593_b200.sharing import share
+    keygen = fss.keygen_cmp if kind == "cmp" else fss.keygen_eq
+    ev = fss.eval_cmp if kind == "cmp" else fss.eval_eq
+    rng = np.random.default_rng(count + n)
+    alpha, k0, k1 = keygen(n, rng, count, device=DEV)
+    path = tmp_path / "k.arnk"
+    keyfile.save_keys(path, k0, k1, chunk=max(1, count // 3))
+    p0, p1 = keyfile.load_keys(path, packed=True, chunk=max(1, count // 2))
+    assert isinstance(p0, fss.PackedKeyBatch) and p0.count == count
+    assert torch.equal(p0.alpha_share.view(torch.int64), k0.alpha_share.view(torch.int64))
+    x = rng.integers(0, 1 << min(n, 63), count, dtype=np.uint64)
+    if n == 64:
+        x = (x << np.uint64(1)) | rng.integers(0, 2, count, dtype=np.uint64)
+    x[::3] = alpha.cpu().numpy()[::3]
+    for party, (pk, uk) in enumerate(((p0, k0), (p1, k1))):
+        assert np.array_equal(ev(party, pk, x), ev(party, uk, x))
+    _same(p1.unpack(), k1)
+    sub = p0.take(np.arange(count)[::-2])
+    assert np.array_equal(ev(0, sub, x[::-2]), ev(0, k0.take(np.arange(count)[::-2]), x[::-2]))
+    if kind == "cmp" and n in (8, 32):
+        if n == 32:
+            lv_p = fss.eval_cmp(0, p0, x, return_levels=True)
+            lv_u = fss.eval_cmp(0, k0, x, return_levels=True)
+            assert np.array_equal(lv_p[1], lv_u[1])
+        ys = share(RingTensor.from_ints(rng.integers(-100, 100, count), n), rng)
+
+        def run(keys):
+            (r0, _), (r1, _) = runtime.run_local_pair(
+                lambda s: fss.sign_protocol(s, ys[s.party], keys[s.party]))
+            return r0.values.numpy(), r1.values.numpy()
+        got = run({0: p0, 1: p1})
+        want = run({0: k0, 1: k1})          # the same keys, unpacked: identical shares
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+        assert p0.consumed.all() and p1.consumed.all()
