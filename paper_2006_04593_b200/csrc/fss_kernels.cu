@@ -299,22 +299,41 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
 // at the payload bytes. Records sit at odd byte offsets: they are read as
 // aligned 32-bit words and realigned with funnel shifts.
 
-// The NB bytes at p (any alignment) as little-endian words o[0..(NB+3)/4):
-// exactly the aligned 32-bit words that hold those bytes are loaded (so the
-// last record of the last element never reads past the payload), then
-// realigned with funnel shifts; bytes of o beyond NB are unspecified.
+// The NB bytes at p (any alignment) as little-endian words o[0..(NB+3)/4),
+// read with 16-byte loads: the lanes of a warp read 32 different records, so
+// each load instruction costs ~32 L1 wavefronts whatever its width -- and the
+// L1 data path is shared with the T-table lookups. Only the aligned 16-byte
+// chunks that hold wanted bytes are loaded (the last record of the last
+// element never reads past the payload); the realignment by the record's
+// offset (uniform across a warp when the record stride is a multiple of 16)
+// is a switch over the 4 word offsets with funnel shifts for the byte offset.
 template <int NB>
 __device__ __forceinline__ void ld_stream(const uint8_t* p, uint32_t (&o)[(NB + 3) / 4]) {
-    constexpr int NO = (NB + 3) / 4, NWMAX = (NB + 6) / 4;   // output words, words touched at worst
-    const uint32_t* a = reinterpret_cast<const uint32_t*>((uintptr_t)p & ~(uintptr_t)3);
-    const uint32_t off = (uint32_t)(uintptr_t)p & 3u;
-    const uint32_t last = (off + NB - 1) >> 2;             // last word holding a wanted byte
-    uint32_t w[NWMAX + 1];
+    constexpr int NO = (NB + 3) / 4, NC = (NB + 30) / 16;   // output words, chunks touched at worst
+    const uint4* a = reinterpret_cast<const uint4*>((uintptr_t)p & ~(uintptr_t)15);
+    const uint32_t off = (uint32_t)(uintptr_t)p & 15u;
+    const uint32_t last = (off + NB - 1) >> 4;             // last chunk holding a wanted byte
+    const uint32_t sh = 8u * (off & 3u);
+    uint32_t w[4 * NC + 4];
 #pragma unroll
-    for (int j = 0; j < NWMAX; j++) w[j] = (uint32_t)j <= last ? __ldg(a + j) : 0u;
-    w[NWMAX] = 0u;
+    for (int c = 0; c < NC; c++) {
+        const uint4 v = (uint32_t)c <= last ? __ldg(a + c) : make_uint4(0, 0, 0, 0);
+        w[4 * c] = v.x;
+        w[4 * c + 1] = v.y;
+        w[4 * c + 2] = v.z;
+        w[4 * c + 3] = v.w;
+    }
 #pragma unroll
-    for (int j = 0; j < NO; j++) o[j] = __funnelshift_r(w[j], w[j + 1], 8 * off);
+    for (int j = 4 * NC; j < 4 * NC + 4; j++) w[j] = 0u;
+#define FSSB_REALIGN(Q)                                                          \
+    _Pragma("unroll") for (int j = 0; j < NO; j++) o[j] = __funnelshift_r(w[j + Q], w[j + Q + 1], sh)
+    switch (off >> 2) {
+        case 0: FSSB_REALIGN(0); break;
+        case 1: FSSB_REALIGN(1); break;
+        case 2: FSSB_REALIGN(2); break;
+        default: FSSB_REALIGN(3); break;
+    }
+#undef FSSB_REALIGN
 }
 
 // A W-byte little-endian ring value at p.
