@@ -34,6 +34,13 @@ a, k0, k1 = fss.keygen_cmp(32, rng, 999)
 keyfile.save_keys("/tmp/sanitize_keys.arnk", k0, k1, chunk=100)
 keyfile.load_keys("/tmp/sanitize_keys.arnk", chunk=64)
 keyfile.load_keys("/tmp/sanitize_keys.arnk", party=1, chunk=333)
+# evaluation straight from payload rows (record loads up to the payload's end)
+for kind, n, N in (("cmp", 32, 999), ("cmp", 12, 77), ("cmp", 63, 33), ("eq", 5, 101), ("eq", 64, 17),
+                   ("eq", 32, 64)):
+    kg = fss.keygen_cmp if kind == "cmp" else fss.keygen_eq
+    a, k0, k1 = kg(n, rng, N)
+    pk = fss.PackedKeyBatch(fss.KIND_CMP if kind == "cmp" else fss.KIND_EQ, 1, n, fss._pack_device(k1))
+    (fss.eval_cmp if kind == "cmp" else fss.eval_eq)(1, pk, a)
 fss.keygen_cmp(16, rng, 64, out_bits=40)
 prg.expand(rng.integers(0, 256, (1000, 16), dtype=np.uint8), 3)
 seeds = torch.randint(0, 256, (1024, 16), dtype=torch.uint8, device="cuda")
