@@ -142,6 +142,9 @@ def run_reference(args, ws, rank):
 
     import oracle
     oracle.build()
+    # all the host threads this process may use: torchrun exports
+    # OMP_NUM_THREADS=1 to every rank, but only rank 0 runs this arm
+    oracle.set_threads(len(os.sched_getaffinity(0)))
     N = 1 << args.cpu_log2n
     rng = np.random.default_rng(1)
     alpha, k0, k1 = oracle.keygen_cmp(N_BITS, rng, N)
@@ -184,6 +187,7 @@ def cpu_baseline_line(log2n: int):
 
     import oracle
     oracle.build()
+    oracle.set_threads(len(os.sched_getaffinity(0)))
     N = 1 << log2n
     rng = np.random.default_rng(1)
     alpha, k0, k1 = oracle.keygen_cmp(N_BITS, rng, N)

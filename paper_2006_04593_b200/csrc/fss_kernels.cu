@@ -863,7 +863,8 @@ int run_host_pipe_pinned(const HostPipe& hp, uint64_t count, Launch launch) {
 // staging copy (2 x 8 B per element) would be slower than the kernel.
 void par_memcpy(void* dst, const void* src, size_t bytes) {
     constexpr size_t kMin = 1 << 20;
-    int nt = omp_get_max_threads();
+    // processors, not omp_get_max_threads(): torchrun exports OMP_NUM_THREADS=1
+    int nt = omp_get_num_procs();
     nt = nt > 8 ? 8 : nt;
     if (bytes < kMin || nt <= 1) {
         memcpy(dst, src, bytes);
