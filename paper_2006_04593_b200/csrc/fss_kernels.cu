@@ -208,7 +208,11 @@ dpf_eval_kernel(int party, int n, uint64_t count, uint64_t ld, const uint8_t* __
 // out_bits <= 32 (hence n <= 32) sigma, leaf and the sum live in 32-bit
 // registers and only the low words of sigma_cw / leaf_cw are read (values
 // < 2^w, little-endian), which removes the 64-bit glue from the ALU pipe.
-template <bool W32>
+#ifndef FSSB_DCF_UNROLL
+#define FSSB_DCF_UNROLL 1
+#endif
+constexpr int kDcfUnroll = FSSB_DCF_UNROLL;   // level-loop unroll (variant sweep)
+template <bool W32, bool LEVELS>
 __global__ void __launch_bounds__(kThreads, 1)
 dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
                 const uint8_t* __restrict__ seed0, const uint8_t* __restrict__ scw,
@@ -238,6 +242,7 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
         W sig = __ldg(sig_w + kStride * e);
         W leaf = __ldg(leaf_w + kStride * e);
 #endif
+#pragma unroll kDcfUnroll
         for (int i = 0; i < n; i++) {
 #if FSSB_PREFETCH_DCF
             const uint64_t offn = (uint64_t)(i + 1 < n ? i + 1 : i) * ld + e;
@@ -266,7 +271,7 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
             const W sigma = lane ^ (sig & (W)(0 - (W)t));
             const W oi = (leaf & (W)(0 - (W)tau)) + sigma;
             acc += oi;
-            if (levels) levels[(uint64_t)i * count + e] = (party ? (0 - (uint64_t)oi) : (uint64_t)oi) & mask;
+            if (LEVELS) levels[(uint64_t)i * count + e] = (party ? (0 - (uint64_t)oi) : (uint64_t)oi) & mask;
             s = xor4(a, and4(cw, tm));
             const uint32_t tn = ((a.w >> 31) ^ (t & (f >> xb))) & 1u;
             s.w &= 0x7FFFFFFFu;
@@ -282,7 +287,7 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
         const W lo = W32 ? (W)s.x : (W)lo64(s);
         const W last = (__ldg(leaf_w + kStride * off) & (W)(0 - (W)t)) + lo;
         acc += last;
-        if (levels) levels[(uint64_t)n * count + e] = (party ? (0 - (uint64_t)last) : (uint64_t)last) & mask;
+        if (LEVELS) levels[(uint64_t)n * count + e] = (party ? (0 - (uint64_t)last) : (uint64_t)last) & mask;
         out[e] = (party ? (0 - (uint64_t)acc) : (uint64_t)acc) & mask;
     }
 }
@@ -816,7 +821,8 @@ int launch_dcf_eval(int party, int n, int out_bits, uint64_t count, uint64_t ld,
     if (!x && (!m_own || !m_peer)) return set_err(kEinval, "need x or both masked messages%s");
     int sms;
     const bool w32 = FSSB_W32 && out_bits <= 32;
-    auto kern = w32 ? dcf_eval_kernel<true> : dcf_eval_kernel<false>;
+    auto kern = levels ? (w32 ? dcf_eval_kernel<true, true> : dcf_eval_kernel<false, true>)
+                       : (w32 ? dcf_eval_kernel<true, false> : dcf_eval_kernel<false, false>);
     if (int rc = prep_launch(kern, &sms)) return rc;
     int threads;
     const int grid = eval_grid(count, sms, &threads);

@@ -20,6 +20,8 @@ VDIR = os.path.join(ROOT, "build", "variants")
 VARIANTS = {
     "default": [],
 }
+# round-1 sweep g (profiles/r01_aes_variants_g_unroll.json): unrolling the DCF
+# level loop x2 = +0.1 % (noise), x4 = -3.3 % (register pressure): off.
 # round-1 sweep b (profiles/r01_aes_variants_b.json): 512/640/768/1024 threads
 # x prefetch; more resident warps win (1024: DCF 92.9 %, DPF 85.5 % of the
 # lookup roof vs 88.2 % / 72.8 % at 512).
