@@ -190,11 +190,11 @@ def sweep(lo, hi):
             ev = fss.eval_cmp if kind == "cmp" else fss.eval_eq
             chunk = min(N, chunk_max)
             rng = np.random.default_rng(log2n)
-            t_kg = ev_time(lambda: keygen(32, rng, chunk, device=DEV), reps=3, warm=1)
+            t_kg = ev_time(lambda: keygen(32, rng, chunk, device=DEV))   # median of 5 after 2 warm-ups
             alpha, k0, k1 = keygen(32, rng, chunk, device=DEV)
             x = alpha.clone()
-            t_e0 = ev_time(lambda: ev(0, k0, x), reps=3, warm=1)
-            t_e1 = ev_time(lambda: ev(1, k1, x), reps=3, warm=1)
+            t_e0 = ev_time(lambda: ev(0, k0, x))
+            t_e1 = ev_time(lambda: ev(1, k1, x))
             rec = (ev(0, k0, x).view(torch.int64) + ev(1, k1, x).view(torch.int64)) & 0xFFFFFFFF
             assert bool((rec == 1).all())
             del alpha, k0, k1, x, rec
