@@ -1,6 +1,6 @@
 """Small, single-kernel-dominated workloads for ncu captures (2^22 elements, n=32).
 
-  python scripts/profile_target.py dcf_eval|dpf_eval|dcf_keygen|dpf_keygen|arnk_pack|arnk_unpack
+  python scripts/profile_target.py dcf_eval|dcf_eval_zerocopy|dpf_eval|dcf_keygen|dpf_keygen|arnk_pack|arnk_unpack
 """
 import os
 import sys
@@ -24,6 +24,8 @@ elif what.startswith("dcf"):
     alpha, k0, k1 = fss.keygen_cmp(32, rng, N, device=dev)
     if what == "dcf_eval":
         fss.eval_cmp(0, k0, alpha)
+    elif what == "dcf_eval_zerocopy":       # x in / shares out in pinned host memory
+        fss.eval_cmp(0, k0, alpha.cpu().pin_memory())
 else:
     alpha, k0, k1 = fss.keygen_eq(32, rng, N, device=dev)
     if what == "dpf_eval":
