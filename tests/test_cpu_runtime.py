@@ -104,3 +104,26 @@ def test_dist_transport_gloo_two_processes():
     assert res[1][0] == [[7, 8, 9], [1 << 40, 3], []]
     assert res[0][1] == 3 and res[0][2] == 3 * 4 + 2 * 8
     assert sorted(g[1] for g in got if len(g) == 2) == ["abort", "abort"]
+
+
+def test_peer_death_mid_round_aborts_not_hangs(monkeypatch):     # reference test_runtime.py:76-86
+    monkeypatch.setenv("ARIANN_TIMEOUT_MS", "500")
+
+    def party0(session):
+        return session.exchange("a", runtime.FRAME_MASKED, torch.zeros(1, dtype=torch.uint8), 1)
+
+    def party1(session):
+        return None          # exits immediately, closing its transport
+
+    with pytest.raises(runtime.SessionAbort):
+        runtime.run_local_pair(party0, party1)
+
+
+def test_large_payload_both_directions_no_deadlock():              # reference test_runtime.py:102-110
+    blob = torch.zeros(2_000_000, dtype=torch.uint8)
+
+    def program(session):
+        return session.exchange("bulk", runtime.FRAME_MASKED, blob, blob.numel()).numel()
+
+    (r0, _), (r1, _) = runtime.run_local_pair(program)
+    assert r0 == blob.numel() and r1 == blob.numel()
