@@ -3,6 +3,8 @@ batch sizes, parties, generator states (incl. numpy's buffered half-word) and
 inputs, the B200 keygen and evaluation equal the C oracle's restatement of
 the reference byte for byte -- keys, rng advance, shares, per-level terms."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -16,7 +18,9 @@ from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E
 
 from paper_2006_04593_b200 import fss  # noqa: E402
 
-SETTINGS = dict(max_examples=60, deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
+# FSS_HYPOTHESIS_EXAMPLES raises the example count for a long soak run
+SETTINGS = dict(max_examples=int(os.environ.get("FSS_HYPOTHESIS_EXAMPLES", "60")), deadline=None,
+                suppress_health_check=[HealthCheck.function_scoped_fixture])
 
 
 def _rng(seed, pre):
