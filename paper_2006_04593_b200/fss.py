@@ -954,6 +954,13 @@ def pack_keys(k0, k1) -> KeyBatch:
         return KeyBatch(KIND_EQ, k0.n_bits, k0.count, _pack_eq(k0), _pack_eq(k1))
     if isinstance(k0, CmpKeyBatch):
         return KeyBatch(KIND_CMP, k0.n_bits, k0.count, _pack_cmp(k0), _pack_cmp(k1))
+    if isinstance(k0, PackedKeyBatch):            # already payload rows: no kernel
+        if k0.kind != k1.kind:
+            raise ValueError("key batches do not form a pair")
+        k0.validate()
+        k1.validate()
+        return KeyBatch(k0.kind, k0.n_bits, k0.count, _dev.to_numpy(k0.payload).tobytes(),
+                        _dev.to_numpy(k1.payload).tobytes())
     raise TypeError(f"cannot pack {type(k0)!r}")
 
 
@@ -1016,6 +1023,12 @@ def audit_keys(k0, k1, tape: FssTape, indices) -> list:
 
     indices = np.asarray(list(indices) if isinstance(indices, range) else indices,
                          dtype=np.int64).reshape(-1)
+    if isinstance(k0, PackedKeyBatch):      # audit the unpacked sample, spend it in the packed batches
+        sub0, sub1 = k0.take(indices).unpack(), k1.take(indices).unpack()
+        k0.consumed[indices] = True
+        k1.consumed[indices] = True
+        bad = audit_keys(sub0, sub1, tape.take(indices), range(indices.size))
+        return [int(indices[j]) for j in bad]
     sub0, sub1 = k0.take(indices), k1.take(indices)
     k0.consumed[indices] = True
     k1.consumed[indices] = True

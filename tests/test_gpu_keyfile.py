@@ -143,3 +143,18 @@ def test_packed_keys_evaluate_like_unpacked(tmp_path, kind, n, count):
         want = run({0: k0, 1: k1})          # the same keys, unpacked: identical shares
         assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
         assert p0.consumed.all() and p1.consumed.all()
+
+
+def test_packed_keys_pack_and_audit(tmp_path):
+    """pack_keys on packed batches reuses the rows (same container bytes), and
+    the cut-and-choose audit works on them (tampering caught, sample spent)."""
+    _, k0, k1, tape = fss.keygen_cmp_with_tape(16, np.random.default_rng(3), 40, device=DEV)
+    path = tmp_path / "k.arnk"
+    keyfile.save_keys(path, k0, k1)
+    p0, p1 = keyfile.load_keys(path, packed=True)
+    assert fss.serialize_keys(fss.pack_keys(p0, p1)) == path.read_bytes()
+    assert fss.audit_keys(p0, p1, tape, [0, 5, 9]) == []
+    assert p0.consumed[[0, 5, 9]].all() and not p0.consumed[1]
+    p1.payload[7, 30] ^= 0x10                       # a correction-word byte of key 7
+    assert fss.audit_keys(p0, p1, tape, range(10, 20)) == []
+    assert fss.audit_keys(p0, p1, tape, [6, 7, 8]) == [7]
