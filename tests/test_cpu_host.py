@@ -169,3 +169,20 @@ def test_take_unused_fast_path_and_fallback():
             assert np.array_equal(got, free[:m])
             ref[free[:m]] = True
             assert np.array_equal(f.consumed, ref)
+
+
+def test_ctypes_signatures_match_header_prototypes():
+    """Every ctypes argtypes list in _lib.SIGNATURES has exactly as many
+    parameters as the C prototype in include/ariann_fss.h declares."""
+    import re
+    from paper_2006_04593_b200 import _lib
+    with open(os.path.join(ROOT, "include", "ariann_fss.h")) as fh:
+        text = re.sub(r"/\*.*?\*/", "", fh.read(), flags=re.S)
+    protos = {}
+    for m in re.finditer(r"\b(?:int|uint64_t|const char\*)\s+(fss_\w+)\s*\(([^)]*)\)\s*;", text):
+        params = m.group(2).strip()
+        protos[m.group(1)] = 0 if params in ("", "void") else params.count(",") + 1
+    assert protos, "no prototypes parsed"
+    for name, argtypes in _lib.SIGNATURES.items():
+        assert name in protos, name
+        assert len(argtypes) == protos[name], (name, len(argtypes), protos[name])
