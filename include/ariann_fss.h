@@ -19,6 +19,9 @@
  *     thread-local error string.
  *   - Return 0 on success; FSS_EINVAL (-> Python ValueError) or FSS_ECUDA
  *     (-> RuntimeError); fss_last_error() gives the calling thread's message.
+ *     Arguments -- ranges, party, and NULL for any required buffer when
+ *     count > 0 -- are validated before any CUDA call, so a bad call never
+ *     faults inside a kernel (which would poison the process's CUDA context).
  */
 #ifndef ARIANN_FSS_H
 #define ARIANN_FSS_H

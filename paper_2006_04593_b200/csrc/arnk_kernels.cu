@@ -702,6 +702,9 @@ int launch(bool pack, int kind, int n, uint64_t count, uint64_t ld, Keys k, uint
         return fssb::set_error(FSS_EINVAL, "ARNK: bad kind or n");
     if (ld < count) return fssb::set_error(FSS_EINVAL, "ARNK: level stride ld < count");
     if (count == 0) return FSS_OK;
+    if (!buf || !k.alpha_share || !k.seed0 || !k.scw || !k.tcw ||
+        (kind == 0 ? !k.cw_final : (!k.sigma_cw || !k.leaf_cw)))
+        return fssb::set_error(FSS_EINVAL, "ARNK: null device pointer");
     cudaStream_t st = (cudaStream_t)stream;
 #if FSSB_ARNK_NAIVE
     const int bs = 256;

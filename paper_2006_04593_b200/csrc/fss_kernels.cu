@@ -20,6 +20,7 @@
 #include <string.h>
 #include <omp.h>
 
+#include <initializer_list>
 #include <type_traits>
 
 #include "../../include/ariann_fss.h"
@@ -717,6 +718,16 @@ int set_err(int code, const char* fmt, const char* a = "") {
     return fssb::set_error(code, buf);
 }
 
+// A NULL device pointer would fault inside the kernel and poison the CUDA
+// context; reject it up front (before any CUDA call) with FSS_EINVAL.
+bool any_null(std::initializer_list<const void*> ptrs) {
+    for (const void* p : ptrs)
+        if (!p) return true;
+    return false;
+}
+#define FSS_REQUIRE(...) \
+    if (any_null({__VA_ARGS__})) return set_err(kEinval, "null device pointer%s")
+
 struct DevInfo {
     int sms = 0;
     bool attr_done = false;
@@ -780,6 +791,7 @@ int fss_aes_mmo_expand(const uint8_t* seeds, uint64_t count, int out_blocks, uin
                        void* stream) {
     if (out_blocks < 2 || out_blocks > 3) return set_err(kEinval, "out_blocks must be 2 or 3%s");
     if (count == 0) return kOk;
+    FSS_REQUIRE(seeds, out);
     int sms;
     if (int rc = prep_launch(expand_kernel, &sms)) return rc;
     int threads;
@@ -801,6 +813,7 @@ int launch_dpf_eval(int party, int n, uint64_t count, uint64_t ld, const uint8_t
     if (n < 1 || n > 64) return set_err(kEinval, "n out of range%s");
     if (count == 0) return kOk;
     if (!x && (!m_own || !m_peer)) return set_err(kEinval, "need x or both masked messages%s");
+    FSS_REQUIRE(seed0, scw, tcw, cw_final, out);
     int sms;
     if (int rc = prep_launch(dpf_eval_kernel, &sms)) return rc;
     int threads;
@@ -819,6 +832,7 @@ int launch_dcf_eval(int party, int n, int out_bits, uint64_t count, uint64_t ld,
         return set_err(kEinval, "need 1 <= n <= out_bits <= 63%s");
     if (count == 0) return kOk;
     if (!x && (!m_own || !m_peer)) return set_err(kEinval, "need x or both masked messages%s");
+    FSS_REQUIRE(seed0, scw, tcw, sigma_cw, leaf_cw, out);
     int sms;
     const bool w32 = FSSB_W32 && out_bits <= 32;
     auto kern = levels ? (w32 ? dcf_eval_kernel<true, true> : dcf_eval_kernel<false, true>)
@@ -1017,6 +1031,7 @@ int fss_dcf_eval_packed(int party, int n, uint64_t count, const uint8_t* payload
     if (n < 1 || n > 63) return set_err(kEinval, "n out of range%s");
     if (count == 0) return kOk;
     if (!x && (!m_own || !m_peer)) return set_err(kEinval, "need x or both masked messages%s");
+    FSS_REQUIRE(payload, out);
     void (*kern)(int, int, uint64_t, const uint8_t*, const uint64_t*, const void*, const void*, uint64_t*);
     switch ((n + 7) / 8) {
         case 1: kern = dcf_eval_packed_kernel<1>; break;
@@ -1043,6 +1058,7 @@ int fss_dpf_eval_packed(int party, int n, uint64_t count, const uint8_t* payload
     if (n < 1 || n > 64) return set_err(kEinval, "n out of range%s");
     if (count == 0) return kOk;
     if (!x && (!m_own || !m_peer)) return set_err(kEinval, "need x or both masked messages%s");
+    FSS_REQUIRE(payload, out);
     void (*kern)(int, int, uint64_t, const uint8_t*, const uint64_t*, const void*, const void*, uint64_t*);
     switch ((n + 7) / 8) {
         case 1: kern = dpf_eval_packed_kernel<1>; break;
@@ -1068,6 +1084,7 @@ int fss_dpf_keygen(int n, uint64_t count, const uint64_t* alpha, const uint64_t*
                    uint64_t* cw_final, uint64_t* alpha1, void* stream) {
     if (n < 1 || n > 64) return set_err(kEinval, "n out of range%s");
     if (count == 0) return kOk;
+    FSS_REQUIRE(alpha, alpha0, s0, s1, scw, tcw, cw_final, alpha1);
     int sms;
     if (int rc = prep_launch(dpf_keygen_kernel, &sms)) return rc;
     int threads;
@@ -1084,6 +1101,7 @@ int fss_dcf_keygen(int n, int out_bits, uint64_t count, const uint64_t* alpha,
     if (n < 1 || n > 63 || out_bits < n || out_bits > 63)
         return set_err(kEinval, "need 1 <= n <= out_bits <= 63%s");
     if (count == 0) return kOk;
+    FSS_REQUIRE(alpha, alpha0, s0, s1, scw, tcw, sigma_cw, leaf_cw, alpha1);
     int sms;
     if (int rc = prep_launch(dcf_keygen_kernel, &sms)) return rc;
     int threads;
@@ -1122,6 +1140,8 @@ int launch_tape(const fss_pcg64_state* st, int n, uint64_t count, int draw_alpha
                 void* stream, uint64_t lo = 0, uint64_t m = ~0ULL) {
     if (m == ~0ULL) m = count - lo;
     if (lo > count || m > count - lo) return set_err(kEinval, "tape slice out of range%s");
+    if (!st || (m && (!s0 || !s1 || (draw_alpha && !alpha) || (draw_alpha0 && !alpha0))))
+        return set_err(kEinval, "null pointer%s");
     TapePlan P;
     P.state_lo = st->state_lo; P.state_hi = st->state_hi;
     P.inc_lo = st->inc_lo; P.inc_hi = st->inc_hi;

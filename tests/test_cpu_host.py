@@ -186,3 +186,22 @@ def test_ctypes_signatures_match_header_prototypes():
     for name, argtypes in _lib.SIGNATURES.items():
         assert name in protos, name
         assert len(argtypes) == protos[name], (name, len(argtypes), protos[name])
+
+
+def test_null_device_pointers_rejected_before_any_cuda_call():
+    """A NULL required pointer returns FSS_EINVAL (ValueError in Python) up
+    front, instead of faulting inside a kernel -- checked without a GPU."""
+    import ctypes
+    from paper_2006_04593_b200 import _lib
+    lib = _lib.load()
+    one = ctypes.c_void_p(16)   # never dereferenced: the call must fail first
+    assert lib.fss_dcf_eval(0, 32, 32, 8, 8, None, one, one, one, one, one, one, None, None) == 1
+    assert b"null" in lib.fss_last_error()
+    assert lib.fss_dpf_eval(0, 32, 8, 8, one, one, one, one, one, None, None) == 1
+    assert lib.fss_dcf_keygen(32, 32, 8, one, one, one, one, one, None, one, one, one, None) == 1
+    assert lib.fss_dpf_keygen(32, 8, one, one, one, one, None, one, one, one, None) == 1
+    assert lib.fss_aes_mmo_expand(None, 8, 3, one, None) == 1
+    assert lib.fss_dcf_eval_packed(0, 32, 8, None, one, None, None, one, None) == 1
+    assert lib.fss_arnk_pack(1, 32, 8, 8, one, one, one, one, None, one, None, one, None) == 1
+    st = _lib.PcgState()
+    assert lib.fss_pcg64_tape(ctypes.byref(st), 32, 8, 1, one, one, None, one, None, None) == 1
