@@ -111,6 +111,7 @@ int fss_ring_op(int op, int n_bits, uint64_t count, const uint64_t* a, const uin
     if (n_bits < 1 || n_bits > 64) return fssb::set_error(FSS_EINVAL, "ring width out of range");
     if (op < FSS_RING_ADD || op > FSS_RING_MASK) return fssb::set_error(FSS_EINVAL, "bad ring op");
     if (count == 0) return FSS_OK;
+    if (!a || !out) return fssb::set_error(FSS_EINVAL, "null device pointer");
     const uint64_t mask = n_bits >= 64 ? ~0ULL : ((1ULL << n_bits) - 1);
     ring_kernel<<<grid_size(count), 256, 0, (cudaStream_t)stream>>>(op, mask, count, a, b, b_scalar, out);
     return done();
@@ -127,6 +128,7 @@ int fss_wire_pack(int op, int n_bits, uint64_t count, const uint64_t* a, const u
     if (op != FSS_RING_ADD && op != FSS_RING_SUB)
         return fssb::set_error(FSS_EINVAL, "wire pack supports add/sub only");
     if (count == 0) return FSS_OK;
+    if (!a || !wire) return fssb::set_error(FSS_EINVAL, "null device pointer");
     const uint64_t mask = n_bits >= 64 ? ~0ULL : ((1ULL << n_bits) - 1);
     wire_pack_kernel<<<grid_size(count), 256, 0, (cudaStream_t)stream>>>(
         op, fss_wire_bytes(n_bits), mask, count, a, b, wire);
@@ -137,6 +139,7 @@ int fss_wire_open(int n_bits, uint64_t count, const void* own, const void* peer,
                   void* stream) {
     if (n_bits < 1 || n_bits > 64) return fssb::set_error(FSS_EINVAL, "ring width out of range");
     if (count == 0) return FSS_OK;
+    if (!own || !out) return fssb::set_error(FSS_EINVAL, "null device pointer");
     const uint64_t mask = n_bits >= 64 ? ~0ULL : ((1ULL << n_bits) - 1);
     wire_open_kernel<<<grid_size(count), 256, 0, (cudaStream_t)stream>>>(
         fss_wire_bytes(n_bits), mask, count, own, peer, out);
@@ -150,6 +153,8 @@ int fss_beaver_mul(int party, int n_bits, uint64_t count, const void* delta_own,
     if (party != 0 && party != 1) return fssb::set_error(FSS_EINVAL, "party must be 0 or 1");
     if (n_bits < 1 || n_bits > 64) return fssb::set_error(FSS_EINVAL, "ring width out of range");
     if (count == 0) return FSS_OK;
+    if (!delta_own || !delta_peer || !eps_own || !eps_peer || !a || !b || !c || !z)
+        return fssb::set_error(FSS_EINVAL, "null device pointer");
     const uint64_t mask = n_bits >= 64 ? ~0ULL : ((1ULL << n_bits) - 1);
     beaver_kernel<<<grid_size(count), 256, 0, (cudaStream_t)stream>>>(
         party, fss_wire_bytes(n_bits), mask, count, delta_own, delta_peer, eps_own, eps_peer, a, b,
