@@ -21,7 +21,9 @@
 #include <omp.h>
 
 #include <initializer_list>
+#include <mutex>
 #include <type_traits>
+#include <vector>
 
 #include "../../include/ariann_fss.h"
 #include "aes_ttable.cuh"
@@ -728,10 +730,17 @@ bool any_null(std::initializer_list<const void*> ptrs) {
 #define FSS_REQUIRE(...) \
     if (any_null({__VA_ARGS__})) return set_err(kEinval, "null device pointer%s")
 
+// Per-device launch facts, set once: the SM count and, per kernel, the 128 KiB
+// dynamic shared-memory opt-in (cudaFuncSetAttribute is per device, and costs
+// a driver call; the online protocols launch small kernels back to back, so it
+// is done on a kernel's first launch on a device only). Two party threads may
+// launch concurrently: the table is guarded by a mutex (the fast path is a
+// short scan of a few entries).
 struct DevInfo {
     int sms = 0;
-    bool attr_done = false;
+    std::vector<const void*> attr_done;   // kernels whose smem opt-in is set
 };
+std::mutex g_dev_mu;
 DevInfo g_dev[64];
 
 template <typename K>
@@ -739,10 +748,20 @@ int prep_launch(K kernel, int* grid) {
     int dev = 0;
     cudaError_t err = cudaGetDevice(&dev);
     if (err != cudaSuccess) return set_err(kEcuda, "cudaGetDevice: %s", cudaGetErrorString(err));
+    const void* key = reinterpret_cast<const void*>(kernel);
+    std::lock_guard<std::mutex> lock(g_dev_mu);
     DevInfo& d = g_dev[dev & 63];
-    if (!d.sms) cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
-    err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fssb::kTableBytes);
-    if (err != cudaSuccess) return set_err(kEcuda, "cudaFuncSetAttribute: %s", cudaGetErrorString(err));
+    if (!d.sms) {
+        err = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+        if (err != cudaSuccess) return set_err(kEcuda, "cudaDeviceGetAttribute: %s", cudaGetErrorString(err));
+    }
+    bool done = false;
+    for (const void* k : d.attr_done) done |= (k == key);
+    if (!done) {
+        err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fssb::kTableBytes);
+        if (err != cudaSuccess) return set_err(kEcuda, "cudaFuncSetAttribute: %s", cudaGetErrorString(err));
+        d.attr_done.push_back(key);
+    }
     *grid = d.sms;
     return kOk;
 }
@@ -812,6 +831,7 @@ int launch_dpf_eval(int party, int n, uint64_t count, uint64_t ld, const uint8_t
     if (party != 0 && party != 1) return set_err(kEinval, "party must be 0 or 1%s");
     if (n < 1 || n > 64) return set_err(kEinval, "n out of range%s");
     if (count == 0) return kOk;
+    if (ld < count) return set_err(kEinval, "level stride ld must be >= count%s");
     if (!x && (!m_own || !m_peer)) return set_err(kEinval, "need x or both masked messages%s");
     FSS_REQUIRE(seed0, scw, tcw, cw_final, out);
     int sms;
@@ -831,6 +851,7 @@ int launch_dcf_eval(int party, int n, int out_bits, uint64_t count, uint64_t ld,
     if (n < 1 || n > 63 || out_bits < n || out_bits > 63)
         return set_err(kEinval, "need 1 <= n <= out_bits <= 63%s");
     if (count == 0) return kOk;
+    if (ld < count) return set_err(kEinval, "level stride ld must be >= count%s");
     if (!x && (!m_own || !m_peer)) return set_err(kEinval, "need x or both masked messages%s");
     FSS_REQUIRE(seed0, scw, tcw, sigma_cw, leaf_cw, out);
     int sms;
@@ -995,6 +1016,7 @@ int fss_dcf_eval_host(int party, int n, int out_bits, uint64_t count, uint64_t l
                       const uint64_t* sigma_cw, const uint64_t* leaf_cw, const uint64_t* x_host,
                       uint64_t* out_host, uint64_t* x_dev, uint64_t* out_dev, uint64_t chunk,
                       uint64_t* stage, void* stream_a, void* stream_b) {
+    if (ld < count) return set_err(kEinval, "level stride ld must be >= count%s");
     const HostPipe hp{x_host, out_host, x_dev, out_dev, chunk,
                       {(cudaStream_t)stream_a, (cudaStream_t)stream_b}, stage};
     return run_host_pipe(hp, count, [&](uint64_t lo, uint64_t m, const uint64_t* xd, uint64_t* od,
@@ -1008,6 +1030,7 @@ int fss_dpf_eval_host(int party, int n, uint64_t count, uint64_t ld, const uint8
                       const uint8_t* scw, const uint8_t* tcw, const uint64_t* cw_final,
                       const uint64_t* x_host, uint64_t* out_host, uint64_t* x_dev, uint64_t* out_dev,
                       uint64_t chunk, uint64_t* stage, void* stream_a, void* stream_b) {
+    if (ld < count) return set_err(kEinval, "level stride ld must be >= count%s");
     const HostPipe hp{x_host, out_host, x_dev, out_dev, chunk,
                       {(cudaStream_t)stream_a, (cudaStream_t)stream_b}, stage};
     return run_host_pipe(hp, count, [&](uint64_t lo, uint64_t m, const uint64_t* xd, uint64_t* od,
@@ -1243,6 +1266,7 @@ int fss_mask_stream(uint64_t seed_lo, uint64_t seed_hi, uint64_t round_idx, uint
 int fss_pcg64_ring_random(const fss_pcg64_state* st, int n_bits, uint64_t count, uint64_t* out,
                           fss_pcg64_state* st_out, void* stream) {
     if (n_bits < 1 || n_bits > 64) return set_err(kEinval, "ring width out of range%s");
+    if (!st || (count && !out)) return set_err(kEinval, "null pointer%s");
     TapePlan P;
     P.state_lo = st->state_lo; P.state_hi = st->state_hi;
     P.inc_lo = st->inc_lo; P.inc_hi = st->inc_hi;

@@ -110,9 +110,20 @@ def read_header(fh, size: int):
 def save_keys(path, k0, k1, chunk: int = CHUNK) -> int:
     """Write the ARNK container of the key pair (byte-identical to
     ``serialize_keys(pack_keys(k0, k1))``); returns the bytes written."""
+    if not isinstance(k0, (fss.EqKeyBatch, fss.CmpKeyBatch, fss.PackedKeyBatch)):
+        raise TypeError(f"cannot save {type(k0).__name__} as an ARNK key file")
     if type(k0) is not type(k1) or k0.n_bits != k1.n_bits or k0.count != k1.count:
         raise ValueError("key batches do not form a pair")
-    kind = KIND_EQ if isinstance(k0, fss.EqKeyBatch) else KIND_CMP
+    packed = isinstance(k0, fss.PackedKeyBatch)
+    if packed:
+        # payload rows already hold the container bytes: streamed as they are
+        if k0.kind != k1.kind:
+            raise ValueError("key batches do not form a pair")
+        k0.validate()
+        k1.validate()
+        kind = k0.kind
+    else:
+        kind = KIND_EQ if isinstance(k0, fss.EqKeyBatch) else KIND_CMP
     if kind == KIND_CMP and k0.out_bits != k0.n_bits:
         raise KeyFormatError("widened-output comparison keys are in-memory only")
     n, count, dev = k0.n_bits, k0.count, k0.device
@@ -135,7 +146,10 @@ def save_keys(path, k0, k1, chunk: int = CHUNK) -> int:
             b = i & 1
             side.wait_stream(torch.cuda.current_stream(dev))
             with torch.cuda.stream(side):
-                buf = fss._pack_device(k.take(slice(lo, hi)))      # column view: no gather
+                if packed:
+                    buf = k.payload[lo:hi]                           # the rows themselves
+                else:
+                    buf = fss._pack_device(k.take(slice(lo, hi)))  # column view: no gather
                 pinned[b][: buf.numel()].copy_(buf.reshape(-1), non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(side)

@@ -175,14 +175,11 @@ class DistTransport:
             raise SessionAbort("transport closed")
         dist = self._dist
         p = frame.payload.to(self.device)
-        hdr = torch.tensor([frame.tag, _DTYPE_CODE[p.dtype], p.numel()], dtype=torch.int64,
-                           device=self.device)
-        peer_hdr = torch.empty(3, dtype=torch.int64, device=self.device)
-        ops = [dist.P2POp(dist.isend, hdr, self.peer, self.group),
-               dist.P2POp(dist.irecv, peer_hdr, self.peer, self.group)]
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
-        tag, code, numel = (int(v) for v in peer_hdr.tolist())
+        tag, code, numel = self._swap_header(frame.tag, _DTYPE_CODE[p.dtype], p.numel())
+        if frame.tag == FRAME_ABORT:
+            # one-way, like the reference's abort frame: the peer raises on our
+            # header and never enters the payload phase, so neither do we
+            return Frame(tag, torch.empty(0, dtype=torch.uint8))
         if tag == FRAME_ABORT:
             raise SessionAbort("peer aborted")
         if code < 0 or code >= len(_DTYPES):
@@ -198,10 +195,27 @@ class DistTransport:
                 w.wait()
         return Frame(tag, out)
 
+    def _swap_header(self, tag: int, code: int, numel: int, timeout=None) -> tuple:
+        dist = self._dist
+        hdr = torch.tensor([tag, code, numel], dtype=torch.int64, device=self.device)
+        peer_hdr = torch.empty(3, dtype=torch.int64, device=self.device)
+        ops = [dist.P2POp(dist.isend, hdr, self.peer, self.group),
+               dist.P2POp(dist.irecv, peer_hdr, self.peer, self.group)]
+        for w in dist.batch_isend_irecv(ops):
+            if timeout is None:
+                w.wait()
+            elif not w.wait(timeout):
+                raise SessionAbort("peer did not take the abort frame")
+        return tuple(int(v) for v in peer_hdr.tolist())
+
     def send_abort(self):
-        # best effort: the peer sees FRAME_ABORT in its next header
+        # best effort, header only: the peer sees FRAME_ABORT in its next header
+        # and raises before any payload is posted on either side
+        import datetime
         try:
-            self.exchange_frames(Frame(FRAME_ABORT, torch.empty(0, dtype=torch.uint8)))
+            if not self._closed:
+                self._swap_header(FRAME_ABORT, 0, 0,
+                                  timeout=datetime.timedelta(seconds=timeout_seconds()))
         except Exception:  # noqa: BLE001
             pass
 
@@ -284,6 +298,7 @@ class PeerTransport:
                             else torch.device("cpu"))
         self._slots, self._peer_ptrs, self._cap, self._round = [], [], 0, 0
         self._closed = False
+        self._aborted = False
         self._grow(capacity)
 
     def _swap(self, t: torch.Tensor) -> torch.Tensor:
@@ -345,6 +360,8 @@ class PeerTransport:
         hdr = torch.tensor([frame.tag, _DTYPE_CODE[p.dtype], p.numel(), nbytes], dtype=torch.int64)
         tag, code, numel, peer_bytes = (int(v) for v in self._swap(hdr).tolist())
         if tag == FRAME_ABORT:
+            # the aborting peer skips the closing barrier: so must we
+            self._aborted = True
             raise SessionAbort("peer aborted")
         if code < 0 or code >= len(_DTYPES):
             raise SessionAbort("corrupt frame header")
@@ -377,7 +394,7 @@ class PeerTransport:
             import ctypes
             self._closed = True
             torch.cuda.current_stream(self.device).synchronize()
-            if not getattr(self, "_aborted", False):
+            if not self._aborted:
                 # the peer may still be reading our slots: leave together
                 self._dist.barrier(group=self.group) if self.group is not None \
                     else self._dist.barrier()

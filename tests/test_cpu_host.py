@@ -205,3 +205,26 @@ def test_null_device_pointers_rejected_before_any_cuda_call():
     assert lib.fss_arnk_pack(1, 32, 8, 8, one, one, one, one, None, one, None, one, None) == 1
     st = _lib.PcgState()
     assert lib.fss_pcg64_tape(ctypes.byref(st), 32, 8, 1, one, one, None, one, None, None) == 1
+
+
+def test_level_stride_and_ring_random_arguments_rejected_without_gpu():
+    """ld < count would make the eval kernels read overlapping level rows, and a
+    NULL generator state would be dereferenced on the host: both are FSS_EINVAL
+    before any CUDA call."""
+    import ctypes
+    from paper_2006_04593_b200 import _lib
+    lib = _lib.load()
+    one = ctypes.c_void_p(16)
+    assert lib.fss_dcf_eval(0, 32, 32, 8, 7, one, one, one, one, one, one, one, None, None) == 1
+    assert b"stride" in lib.fss_last_error()
+    assert lib.fss_dpf_eval(0, 32, 8, 7, one, one, one, one, one, one, None) == 1
+    assert lib.fss_dcf_eval_masked(0, 32, 32, 8, 4, one, one, one, one, one, one, one, one, None) == 1
+    assert lib.fss_dpf_eval_masked(0, 32, 8, 4, one, one, one, one, one, one, one, None) == 1
+    assert lib.fss_dcf_eval_host(0, 32, 32, 8, 7, one, one, one, one, one, one, one, one, one, 4,
+                                 None, None, None) == 1
+    assert lib.fss_dpf_eval_host(0, 32, 8, 7, one, one, one, one, one, one, one, one, 4,
+                                 None, None, None) == 1
+    assert lib.fss_pcg64_ring_random(None, 32, 8, one, None, None) == 1
+    assert b"null" in lib.fss_last_error()
+    st = _lib.PcgState()
+    assert lib.fss_pcg64_ring_random(ctypes.byref(st), 32, 8, None, None, None) == 1

@@ -127,3 +127,55 @@ def test_large_payload_both_directions_no_deadlock():              # reference t
 
     (r0, _), (r1, _) = runtime.run_local_pair(program)
     assert r0 == blob.numel() and r1 == blob.numel()
+
+
+def _abort_worker(rank, port, q):
+    import datetime
+    import time
+
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    # a process-group timeout far above the test's bound: a hang would show
+    dist.init_process_group("gloo", rank=rank, world_size=2, timeout=datetime.timedelta(seconds=90))
+    try:
+        def prog(session):
+            session.exchange("a", runtime.FRAME_MASKED, torch.zeros(4, dtype=torch.int32), 4)
+            if session.party == 1:
+                raise ValueError("party 1 fails mid-program")
+            # party 0 announces a large payload; the aborting side must not post
+            # a receive for it (it would block until the group timeout)
+            return session.exchange("b", runtime.FRAME_MASKED, torch.zeros(1 << 16, dtype=torch.int64),
+                                    1 << 16)
+        t0 = time.time()
+        try:
+            runtime.run_dist_party(rank, 1 - rank, prog)
+            outcome = "no-error"
+        except runtime.SessionAbort:
+            outcome = "abort"
+        except ValueError:
+            outcome = "raised"
+        dt = time.time() - t0
+        # the pair is still in step: a fresh session exchanges normally
+        res, _ = runtime.run_dist_party(
+            rank, 1 - rank,
+            lambda s: int(s.exchange("c", runtime.FRAME_MASKED, torch.full((3,), 5 + rank,
+                                                                            dtype=torch.int32), 3)[0]))
+        q.put((rank, outcome, dt, res))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dist_abort_mid_program_fails_fast():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_abort_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got[0][1] == "abort" and got[1][1] == "raised"
+    assert got[0][2] < 30 and got[1][2] < 30          # not the 90 s group timeout
+    assert got[0][3] == 6 and got[1][3] == 5

@@ -158,3 +158,18 @@ def test_packed_keys_pack_and_audit(tmp_path):
     p1.payload[7, 30] ^= 0x10                       # a correction-word byte of key 7
     assert fss.audit_keys(p0, p1, tape, range(10, 20)) == []
     assert fss.audit_keys(p0, p1, tape, [6, 7, 8]) == [7]
+
+
+@pytest.mark.parametrize("kind,n,count", [("cmp", 32, 1000), ("eq", 16, 333)])
+def test_save_packed_keys(tmp_path, kind, n, count):
+    """save_keys on packed batches streams the payload rows as they are: the file
+    equals the one written from the typed batches, for both kinds."""
+    keygen = fss.keygen_cmp if kind == "cmp" else fss.keygen_eq
+    _, k0, k1 = keygen(n, np.random.default_rng(count), count, device=DEV)
+    a, b = tmp_path / "a.arnk", tmp_path / "b.arnk"
+    keyfile.save_keys(a, k0, k1, chunk=300)
+    p0, p1 = keyfile.load_keys(a, packed=True)
+    assert keyfile.save_keys(b, p0, p1, chunk=77) == a.stat().st_size
+    assert b.read_bytes() == a.read_bytes()
+    with pytest.raises(TypeError):
+        keyfile.save_keys(b, object(), object())

@@ -140,3 +140,30 @@ def test_single_use_keys_and_desync():
         return fss.sign_protocol(session, me, keys)   # keys are spent
     with pytest.raises(fss.KeyExhaustedError):
         runtime.run_local_pair(prog)
+
+
+def test_dealer_material_survives_cross_stream_release():
+    """Material generated on party 0's stream and consumed on party 1's must not
+    be recycled by party 0's allocator pool while party 1's kernels still read
+    it: the dealer marks every tensor as used on the consumer stream."""
+    M = 1 << 20
+    d = dealer.make_dealer(32, seed=9)
+    s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(s0):
+        k0 = d.for_party(0).cmp_keys(M)
+    x = torch.from_numpy(np.random.default_rng(1).integers(0, 1 << 32, M, dtype=np.uint64)
+                         .view(np.int64)).cuda().view(torch.uint64)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        k1 = d.for_party(1).cmp_keys(M)
+        want = fss.eval_cmp(1, k1, x).clone()
+        s1.synchronize()
+        outs = [fss.eval_cmp(1, k1, x) for _ in range(30)]    # ~tens of ms of reads queued
+    del k0, k1
+    with torch.cuda.stream(s0):                               # reuse party 0's pool at once
+        junk = [torch.full((32, M, 16), 0xFF, dtype=torch.uint8, device="cuda") for _ in range(2)]
+        junk += [torch.full((33, M), -1, dtype=torch.int64, device="cuda") for _ in range(2)]
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o.view(torch.int64), want.view(torch.int64))
+    del junk
