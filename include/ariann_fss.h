@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define FSS_ABI_VERSION 3
+#define FSS_ABI_VERSION 4
 #define FSS_OK 0
 #define FSS_EINVAL 1
 #define FSS_ECUDA 2
@@ -60,12 +60,6 @@ int fss_aes_mmo_expand(const uint8_t* seeds, uint64_t count, int out_blocks, uin
  * top bit cleared, 2-block MMO expansion -> 4 u64 lanes. */
 int fss_mask_stream(uint64_t seed_lo, uint64_t seed_hi, uint64_t round_idx, uint64_t count,
                     int n_bits, uint64_t* out, void* stream);
-
-/* Same result as fss_aes_mmo_expand through the bitsliced AES
- * (csrc/aes_bitsliced.cuh) instead of T-tables: the measured alternative
- * SURVEY.md 8d proposed. count must be a multiple of 32. */
-int fss_aes_mmo_expand_bitsliced(const uint8_t* seeds, uint64_t count, int out_blocks, uint8_t* out,
-                                 void* stream);
 
 /* fss._sample_tape (fss.py:292-303) through numpy's PCG64 Generator
  * (_uniform_ring fss.py:47-51, random_seeds prg.py:36-40) for 1 <= n <= 63:

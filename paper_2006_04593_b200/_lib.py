@@ -33,13 +33,12 @@ class Peaks(ctypes.Structure):
 
 
 # name -> argtypes (all return int status unless listed in _RESTYPE)
-ABI_VERSION = 3   # include/ariann_fss.h FSS_ABI_VERSION
+ABI_VERSION = 4   # include/ariann_fss.h FSS_ABI_VERSION
 
 SIGNATURES = {
     "fss_abi_version": [],
     "fss_last_error": [],
     "fss_aes_mmo_expand": [_vp, _u64, _int, _vp, _vp],
-    "fss_aes_mmo_expand_bitsliced": [_vp, _u64, _int, _vp, _vp],
     "fss_mask_stream": [_u64, _u64, _u64, _u64, _int, _vp, _vp],
     "fss_pcg64_tape": [ctypes.POINTER(PcgState), _int, _u64, _int, _vp, _vp, _vp, _vp,
                        ctypes.POINTER(PcgState), _vp],

@@ -192,6 +192,42 @@ __device__ __forceinline__ void mmo_half(const Tab& tb, U4 s, uint32_t hm, uint3
     hi = lop3_xor3(last_col(tb, a1, a2, a3, a0), k_hi, s_hi);
 }
 
+// ---- per-lane key among all three fixed keys (lane-pair evaluation) ----
+// rk = RK1 ^ (ma & (RK1 ^ RK2)) ^ (mb & (RK1 ^ RK3)): ma selects k2, mb selects
+// k3 (never both). Lanes of one warp then run ONE instruction stream while
+// encrypting under different keys -- one more LOP3 per column than SEL.
+__device__ __forceinline__ uint32_t rk3(int w, uint32_t ma, uint32_t mb) {
+    return lop3_xor_and(lop3_xor_and(kRK[0][w], ma, kRK[0][w] ^ kRK[1][w]), mb, kRK[0][w] ^ kRK[2][w]);
+}
+
+__device__ __forceinline__ U4 mmo3(const Tab& tb, U4 s, uint32_t ma, uint32_t mb) {
+    uint32_t c0 = s.x ^ rk3(0, ma, mb), c1 = s.y ^ rk3(1, ma, mb);
+    uint32_t c2 = s.z ^ rk3(2, ma, mb), c3 = s.w ^ rk3(3, ma, mb);
+#pragma unroll
+    for (int r = 1; r < 10; r++) {
+#define FSSB_MIX3(A, B, C, D, W)                                                                   \
+    lop3_xor_and(lop3_xor_and(lop3_xor3(lop3_xor3(T<0, 0>(tb, A), T<1, 1>(tb, B), T<2, 2>(tb, C)),  \
+                                        T<3, 3>(tb, D), kRK[0][W]),                                 \
+                              ma, kRK[0][W] ^ kRK[1][W]),                                           \
+                 mb, kRK[0][W] ^ kRK[2][W])
+        const uint32_t n0 = FSSB_MIX3(c0, c1, c2, c3, 4 * r + 0);
+        const uint32_t n1 = FSSB_MIX3(c1, c2, c3, c0, 4 * r + 1);
+        const uint32_t n2 = FSSB_MIX3(c2, c3, c0, c1, 4 * r + 2);
+        const uint32_t n3 = FSSB_MIX3(c3, c0, c1, c2, 4 * r + 3);
+#undef FSSB_MIX3
+        c0 = n0;
+        c1 = n1;
+        c2 = n2;
+        c3 = n3;
+    }
+    U4 o;
+    o.x = lop3_xor3(last_col(tb, c0, c1, c2, c3), rk3(40, ma, mb), s.x);
+    o.y = lop3_xor3(last_col(tb, c1, c2, c3, c0), rk3(41, ma, mb), s.y);
+    o.z = lop3_xor3(last_col(tb, c2, c3, c0, c1), rk3(42, ma, mb), s.z);
+    o.w = lop3_xor3(last_col(tb, c3, c0, c1, c2), rk3(43, ma, mb), s.w);
+    return o;
+}
+
 // Matyas-Meyer-Oseas block: AES_k(s) XOR s  (reference prg.expand, prg.py:43-60).
 template <int KEY, bool SEL>
 __device__ __forceinline__ U4 mmo(const Tab& tb, U4 s, uint32_t m) {

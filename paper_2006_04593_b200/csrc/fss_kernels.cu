@@ -54,6 +54,15 @@ namespace {
 #ifndef FSSB_THREADS
 #define FSSB_THREADS 1024
 #endif
+// Batches of at most this many elements per SM use the lane-pair DCF eval
+// kernel (0 disables it).
+#ifndef FSSB_PAIR_MAX_PER_SM
+#define FSSB_PAIR_MAX_PER_SM 0
+#endif
+// ... and of keygen (lane-pair keygen kernel; 0 disables it)
+#ifndef FSSB_KEYGEN_PAIR_MAX_PER_SM
+#define FSSB_KEYGEN_PAIR_MAX_PER_SM 0
+#endif
 // Eval kernels: 32 warps per SM (64 registers) hide the LDS / LDG latency best
 // (profiles/r01_aes_variants_b.json: 512 -> 1024 threads = +5 % DCF, +17 % DPF).
 constexpr int kThreads = FSSB_THREADS;
@@ -292,6 +301,77 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
         acc += last;
         if (LEVELS) levels[(uint64_t)n * count + e] = (party ? (0 - (uint64_t)last) : (uint64_t)last) & mask;
         out[e] = (party ? (0 - (uint64_t)acc) : (uint64_t)acc) & mask;
+    }
+}
+
+// ------------------------------------------------- DCF eval, lane pairs
+// Small batches (config 1: 2^16 keys = 443 per SM) leave the one-lane kernel
+// with too few warps per SM to keep the LDS pipe busy. Here a PAIR of lanes
+// evaluates one element: the even lane encrypts the child block (key k1/k2 by
+// x_i), the odd lane the sigma/tau block (k3) -- one instruction stream with a
+// per-lane key (mmo3) -- and the even lane's child block is shuffled to its
+// partner, so both lanes carry the same (s, t) down the tree. The odd lane
+// accumulates and stores the output. Per level 2 x 160 lookups (+8 over the
+// half-block trick) and 4 SHFL, for twice the warps per element.
+template <bool W32>
+__global__ void __launch_bounds__(kThreads, 1)
+dcf_eval_pair_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
+                     const uint8_t* __restrict__ seed0, const uint8_t* __restrict__ scw,
+                     const uint8_t* __restrict__ tcw, const uint64_t* __restrict__ sigma_cw,
+                     const uint64_t* __restrict__ leaf_cw, const uint64_t* __restrict__ x,
+                     const void* __restrict__ m_own, const void* __restrict__ m_peer,
+                     uint64_t* __restrict__ out) {
+    using W = typename std::conditional<W32, uint32_t, uint64_t>::type;
+    extern __shared__ uint32_t tab[];
+    fssb::fill_tables(tab);
+    __syncthreads();
+    const fssb::Tab tb = fssb::make_tab(tab);
+    const uint64_t nmask = ring_mask(n);
+    const uint64_t mask = ring_mask(out_bits);
+    const W* __restrict__ sig_w = reinterpret_cast<const W*>(sigma_cw);
+    const W* __restrict__ leaf_w = reinterpret_cast<const W*>(leaf_cw);
+    constexpr int kStride = W32 ? 2 : 1;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t odd = lane & 1;
+    const uint32_t pm = 3u << (lane & ~1u);       // the pair's shuffle mask
+    const uint32_t mb = 0u - odd;                  // odd lane: key k3
+    const Span sp = cta_span(count);
+    for (uint64_t e = sp.lo + (threadIdx.x >> 1); e < sp.hi; e += blockDim.x >> 1) {
+        U4 s = ld16(seed0 + 16 * e);
+        uint32_t t = party;
+        W acc = 0;
+        const uint64_t xe = load_x(x, m_own, m_peer, n, e) & nmask;
+        for (int i = 0; i < n; i++) {
+            const uint64_t off = (uint64_t)i * ld + e;
+            const U4 cw = ld16(scw + 16 * off);
+            const uint32_t f = __ldg(tcw + off);
+            const uint32_t xb = (uint32_t)(xe >> (n - 1 - i)) & 1u;
+            const U4 b = fssb::mmo3(tb, s, (0u - xb) & ~mb, mb);
+            U4 a;
+            a.x = __shfl_sync(pm, b.x, lane & ~1u);
+            a.y = __shfl_sync(pm, b.y, lane & ~1u);
+            a.z = __shfl_sync(pm, b.z, lane & ~1u);
+            a.w = __shfl_sync(pm, b.w, lane & ~1u);
+            if (odd) {   // sigma/tau lane x_i of the third block (slice_cmp, prg.py:99-119)
+                const W sig = __ldg(sig_w + kStride * off);
+                const W leaf = __ldg(leaf_w + kStride * off);
+                const uint32_t lane_lo = xb ? b.z : b.x, lane_hi = xb ? b.w : b.y;
+                const W lv = W32 ? (W)lane_lo : (W)(((uint64_t)lane_hi << 32) | lane_lo);
+                const uint32_t tau = ((lane_hi >> 31) ^ (t & (f >> (2 + xb)))) & 1u;
+                const W sigma = lv ^ (sig & (W)(0 - (W)t));
+                acc += (leaf & (W)(0 - (W)tau)) + sigma;
+            }
+            s = xor4(a, and4(cw, 0u - t));
+            const uint32_t tn = ((a.w >> 31) ^ (t & (f >> xb))) & 1u;
+            s.w &= 0x7FFFFFFFu;
+            t = tn;
+        }
+        if (odd) {
+            const uint64_t off = (uint64_t)n * ld + e;
+            const W lo = W32 ? (W)s.x : (W)lo64(s);
+            acc += (__ldg(leaf_w + kStride * off) & (W)(0 - (W)t)) + lo;
+            out[e] = (party ? (0 - (uint64_t)acc) : (uint64_t)acc) & mask;
+        }
     }
 }
 
@@ -547,6 +627,118 @@ dcf_keygen_kernel(int n, int out_bits, uint64_t count, const uint64_t* __restric
         const uint64_t v = (1 - (lo64(s0) & mask) + (lo64(s1) & mask)) & mask;
         leaf_cw[(uint64_t)n * count + e] = t1 ? ((0 - v) & mask) : v;
         alpha1[e] = (al - alpha0[e]) & nmask;
+    }
+}
+
+// ---------------------------------------------------- keygen, lane pairs
+// Small batches: a PAIR of lanes deals one key pair -- the even lane walks
+// party 0's seed, the odd lane party 1's (same three fixed keys: one
+// instruction stream), so each lane encrypts 3 (DCF) or 2 (DPF) blocks per
+// level instead of 6 / 4. Per level the partners swap what the correction
+// words need (the off-path child seed, the sigma/tau block, the t bits) by
+// shuffles and compute identical correction words; the even lane stores the
+// seed / t corrections, the odd lane sigma and the leaf word.
+constexpr int kPairKeygenThreads = 1024;
+
+template <bool CMP>
+__global__ void __launch_bounds__(kPairKeygenThreads, 1)
+keygen_pair_kernel(int n, int out_bits, uint64_t count, const uint64_t* __restrict__ alpha,
+                   const uint64_t* __restrict__ alpha0, const uint8_t* __restrict__ s0_init,
+                   const uint8_t* __restrict__ s1_init, uint8_t* __restrict__ scw,
+                   uint8_t* __restrict__ tcw, uint64_t* __restrict__ sigma_cw,
+                   uint64_t* __restrict__ leaf_cw, uint64_t* __restrict__ cw_final,
+                   uint64_t* __restrict__ alpha1) {
+    extern __shared__ uint32_t tab[];
+    fssb::fill_tables(tab);
+    __syncthreads();
+    const fssb::Tab tb = fssb::make_tab(tab);
+    const uint64_t nmask = ring_mask(n);
+    const uint64_t mask = ring_mask(out_bits);
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t p = lane & 1;                 // the party this lane walks
+    const uint32_t pm = 3u << (lane & ~1u);
+    const uint32_t q = lane ^ 1u;                // partner lane
+    const Span sp = cta_span(count);
+    for (uint64_t e = sp.lo + (threadIdx.x >> 1); e < sp.hi; e += blockDim.x >> 1) {
+        U4 s = ld16((p ? s1_init : s0_init) + 16 * e);
+        uint32_t t = p;
+        const uint64_t al = alpha[e] & nmask;
+        for (int i = 0; i < n; i++) {
+            const uint32_t a = (uint32_t)(al >> (n - 1 - i)) & 1u;
+            U4 l = fssb::mmo<0, false>(tb, s, 0), r = fssb::mmo<1, false>(tb, s, 0);
+            const uint32_t tl = l.w >> 31, tr = r.w >> 31;
+            l.w &= 0x7FFFFFFFu;
+            r.w &= 0x7FFFFFFFu;
+            // the off-path child of both parties gives the seed correction
+            const U4 side = a ? l : r;
+            U4 cws;
+            cws.x = side.x ^ __shfl_sync(pm, side.x, q);
+            cws.y = side.y ^ __shfl_sync(pm, side.y, q);
+            cws.z = side.z ^ __shfl_sync(pm, side.z, q);
+            cws.w = side.w ^ __shfl_sync(pm, side.w, q);
+            uint32_t g_x = 0, g_y = 0, g_z = 0, g_w = 0, h_x = 0, h_y = 0, h_z = 0, h_w = 0;
+            if (CMP) {
+                const U4 g = fssb::mmo<2, false>(tb, s, 0);
+                g_x = g.x; g_y = g.y; g_z = g.z; g_w = g.w;
+                h_x = __shfl_sync(pm, g.x, q);
+                h_y = __shfl_sync(pm, g.y, q);
+                h_z = __shfl_sync(pm, g.z, q);
+                h_w = __shfl_sync(pm, g.w, q);
+            }
+            const uint32_t bits = tl | (tr << 1) | (t << 2);
+            const uint32_t pb = __shfl_sync(pm, bits, q);
+            // (party 0, party 1) views of the exchanged values
+            const uint32_t b0 = p ? pb : bits, b1 = p ? bits : pb;
+            const uint32_t tl0 = b0 & 1u, tr0 = (b0 >> 1) & 1u, t0 = (b0 >> 2) & 1u;
+            const uint32_t tl1 = b1 & 1u, tr1 = (b1 >> 1) & 1u, t1 = (b1 >> 2) & 1u;
+            const uint32_t cw_tl = tl0 ^ tl1 ^ 1u ^ a;
+            const uint32_t cw_tr = tr0 ^ tr1 ^ a;
+            const uint64_t off = (uint64_t)i * count + e;
+            if (!p) {
+                st16(scw + 16 * off, cws);
+            }
+            uint32_t tbyte = cw_tl | (cw_tr << 1);
+            if (CMP) {
+                const uint32_t G0x = p ? h_x : g_x, G0y = p ? h_y : g_y, G0z = p ? h_z : g_z, G0w = p ? h_w : g_w;
+                const uint32_t G1x = p ? g_x : h_x, G1y = p ? g_y : h_y, G1z = p ? g_z : h_z, G1w = p ? g_w : h_w;
+                const uint64_t gl0 = (((uint64_t)G0y << 32) | G0x) & mask, gr0 = (((uint64_t)G0w << 32) | G0z) & mask;
+                const uint64_t gl1 = (((uint64_t)G1y << 32) | G1x) & mask, gr1 = (((uint64_t)G1w << 32) | G1z) & mask;
+                const uint32_t ul0 = G0y >> 31, ur0 = G0w >> 31, ul1 = G1y >> 31, ur1 = G1w >> 31;
+                // sigma collapses on the stay side (alpha bit), fss.py:245-249
+                const uint64_t cw_sig = a ? (gr0 ^ gr1) : (gl0 ^ gl1);
+                const uint32_t cw_ul = ul0 ^ ul1 ^ a;
+                const uint32_t cw_ur = ur0 ^ ur1 ^ 1u ^ a;
+                tbyte |= (cw_ul << 2) | (cw_ur << 3);
+                if (p) {
+                    // leaf word from the exit side after correction, fss.py:268-273
+                    sigma_cw[off] = cw_sig;
+                    const uint64_t g0x = (a ? gl0 : gr0) ^ (t0 ? cw_sig : 0);
+                    const uint64_t g1x = (a ? gl1 : gr1) ^ (t1 ? cw_sig : 0);
+                    const uint32_t u1x = (a ? ul1 : ur1) ^ (t1 & (a ? cw_ul : cw_ur));
+                    const uint64_t leaf = ((uint64_t)a - g0x + g1x) & mask;
+                    leaf_cw[off] = u1x ? ((0 - leaf) & mask) : leaf;
+                }
+            }
+            if (!p) tcw[off] = (uint8_t)tbyte;
+            // advance this lane's party along alpha
+            s = xor4(sel4(a, r, l), and4(cws, 0u - t));
+            t = (a ? tr : tl) ^ (t & (a ? cw_tr : cw_tl));
+        }
+        const uint32_t o_lo = __shfl_sync(pm, s.x, q), o_hi = __shfl_sync(pm, s.y, q);
+        const uint32_t o_t = __shfl_sync(pm, t, q);
+        if (p) {   // this lane holds (s1, t1), its partner (s0, t0)
+            const uint64_t s0r = ((uint64_t)o_hi << 32) | o_lo;
+            if (CMP) {
+                const uint64_t v = (1 - (s0r & mask) + (lo64(s) & mask)) & mask;
+                leaf_cw[(uint64_t)n * count + e] = t ? ((0 - v) & mask) : v;
+            } else {
+                const uint64_t v = (1 - s0r + lo64(s)) & mask;
+                cw_final[e] = t ? ((0 - v) & mask) : v;
+            }
+        } else {
+            (void)o_t;
+            alpha1[e] = (al - alpha0[e]) & nmask;
+        }
     }
 }
 
@@ -856,6 +1048,18 @@ int launch_dcf_eval(int party, int n, int out_bits, uint64_t count, uint64_t ld,
     FSS_REQUIRE(seed0, scw, tcw, sigma_cw, leaf_cw, out);
     int sms;
     const bool w32 = FSSB_W32 && out_bits <= 32;
+    if (!levels && FSSB_PAIR_MAX_PER_SM > 0) {
+        // small batch: two lanes per element (dcf_eval_pair_kernel)
+        auto pk = w32 ? dcf_eval_pair_kernel<true> : dcf_eval_pair_kernel<false>;
+        if (int rc = prep_launch(pk, &sms)) return rc;
+        if (count <= (uint64_t)sms * FSSB_PAIR_MAX_PER_SM) {
+            int threads;
+            const int grid = balanced_grid(2 * count, sms, kThreads, &threads);
+            pk<<<grid, threads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+                party, n, out_bits, count, ld, seed0, scw, tcw, sigma_cw, leaf_cw, x, m_own, m_peer, out);
+            return check_launch();
+        }
+    }
     auto kern = levels ? (w32 ? dcf_eval_kernel<true, true> : dcf_eval_kernel<false, true>)
                        : (w32 ? dcf_eval_kernel<true, false> : dcf_eval_kernel<false, false>);
     if (int rc = prep_launch(kern, &sms)) return rc;
@@ -1109,6 +1313,16 @@ int fss_dpf_keygen(int n, uint64_t count, const uint64_t* alpha, const uint64_t*
     if (count == 0) return kOk;
     FSS_REQUIRE(alpha, alpha0, s0, s1, scw, tcw, cw_final, alpha1);
     int sms;
+    if (FSSB_KEYGEN_PAIR_MAX_PER_SM > 0) {
+        if (int rc = prep_launch(keygen_pair_kernel<false>, &sms)) return rc;
+        if (count <= (uint64_t)sms * FSSB_KEYGEN_PAIR_MAX_PER_SM) {
+            int threads;
+            const int grid = balanced_grid(2 * count, sms, kPairKeygenThreads, &threads);
+            keygen_pair_kernel<false><<<grid, threads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+                n, n, count, alpha, alpha0, s0, s1, scw, tcw, nullptr, nullptr, cw_final, alpha1);
+            return check_launch();
+        }
+    }
     if (int rc = prep_launch(dpf_keygen_kernel, &sms)) return rc;
     int threads;
     const int grid = balanced_grid(count, sms, kKeygenThreads, &threads);
@@ -1126,6 +1340,16 @@ int fss_dcf_keygen(int n, int out_bits, uint64_t count, const uint64_t* alpha,
     if (count == 0) return kOk;
     FSS_REQUIRE(alpha, alpha0, s0, s1, scw, tcw, sigma_cw, leaf_cw, alpha1);
     int sms;
+    if (FSSB_KEYGEN_PAIR_MAX_PER_SM > 0) {
+        if (int rc = prep_launch(keygen_pair_kernel<true>, &sms)) return rc;
+        if (count <= (uint64_t)sms * FSSB_KEYGEN_PAIR_MAX_PER_SM) {
+            int threads;
+            const int grid = balanced_grid(2 * count, sms, kPairKeygenThreads, &threads);
+            keygen_pair_kernel<true><<<grid, threads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+                n, out_bits, count, alpha, alpha0, s0, s1, scw, tcw, sigma_cw, leaf_cw, nullptr, alpha1);
+            return check_launch();
+        }
+    }
     if (int rc = prep_launch(dcf_keygen_kernel, &sms)) return rc;
     int threads;
     const int grid = balanced_grid(count, sms, kKeygenThreads, &threads);

@@ -99,8 +99,12 @@ def run(log2n: int):
     res = torch.empty((M, 48), dtype=torch.uint8, device=dev)
     ref = torch.empty_like(res)
     main = _lib.load()
+    sys.path.insert(0, os.path.join(ROOT, "scripts", "research", "bitsliced"))
+    import build as bs_build                      # research record, not in the product ABI
+    bs = ctypes.CDLL(bs_build.build())
+    bs.fss_aes_mmo_expand_bitsliced.argtypes = _lib.SIGNATURES["fss_aes_mmo_expand"]
     for name, fn in (("expand_ttable", main.fss_aes_mmo_expand),
-                     ("expand_bitsliced", main.fss_aes_mmo_expand_bitsliced)):
+                     ("expand_bitsliced", bs.fss_aes_mmo_expand_bitsliced)):
         def go(fn=fn, o=(ref if name == "expand_ttable" else res)):
             assert fn(_dev.ptr(seeds), M, 3, _dev.ptr(o), stream.cuda_stream) == 0
         go()

@@ -1,14 +1,21 @@
-// Bitsliced AES-MMO expand (prg.expand, prg.py:43-60) -- the measured
-// alternative to the T-table expand_kernel. One thread owns 32 consecutive
+// RESEARCH RECORD, not part of the product library: bitsliced AES-MMO expand
+// (prg.expand, prg.py:43-60) -- the measured alternative to the T-table
+// expand_kernel (7x slower on B200, 255 registers).
+// Built on demand into scripts/_variants/libfss_bitsliced.so by
+// scripts/research/bitsliced/build.py for tests/test_gpu_fss.py and
+// scripts/aes_variants.py. One thread owns 32 consecutive
 // seeds; for each output block it transposes them into 128 bit-slices,
 // runs the fixed-key bitsliced AES (aes_bitsliced.cuh), transposes back and
 // applies the MMO feed-forward. Pure ALU work (LOP3 / SHF): no tables.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include "../../include/ariann_fss.h"
 #include "aes_bitsliced.cuh"
-#include "common.cuh"
+
+// status codes of include/ariann_fss.h (this library is standalone)
+#define BS_OK 0
+#define BS_EINVAL 1
+#define BS_ECUDA 2
 
 namespace {
 
@@ -56,9 +63,9 @@ bs_expand_kernel(const uint8_t* __restrict__ seeds, uint64_t groups, int blocks,
 
 extern "C" int fss_aes_mmo_expand_bitsliced(const uint8_t* seeds, uint64_t count, int out_blocks,
                                             uint8_t* out, void* stream) {
-    if (out_blocks < 2 || out_blocks > 3) return fssb::set_error(FSS_EINVAL, "out_blocks must be 2 or 3");
-    if (count % 32) return fssb::set_error(FSS_EINVAL, "bitsliced expand needs count % 32 == 0");
-    if (count == 0) return FSS_OK;
+    if (out_blocks < 2 || out_blocks > 3) return BS_EINVAL;
+    if (count % 32) return BS_EINVAL;   // 32 seeds per thread
+    if (count == 0) return BS_OK;
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -69,5 +76,5 @@ extern "C" int fss_aes_mmo_expand_bitsliced(const uint8_t* seeds, uint64_t count
     bs_expand_kernel<<<(unsigned)grid, kBsThreads, 0, (cudaStream_t)stream>>>(seeds, groups, out_blocks,
                                                                                out);
     const cudaError_t err = cudaGetLastError();
-    return err == cudaSuccess ? FSS_OK : fssb::set_error(FSS_ECUDA, cudaGetErrorString(err));
+    return err == cudaSuccess ? BS_OK : BS_ECUDA;
 }

@@ -45,7 +45,7 @@ fss.keygen_cmp(16, rng, 64, out_bits=40)
 prg.expand(rng.integers(0, 256, (1000, 16), dtype=np.uint8), 3)
 seeds = torch.randint(0, 256, (1024, 16), dtype=torch.uint8, device="cuda")
 out = torch.empty((1024, 48), dtype=torch.uint8, device="cuda")
-_lib.call("fss_aes_mmo_expand_bitsliced", _dev.ptr(seeds), 1024, 3, _dev.ptr(out),
+_lib.call("fss_aes_mmo_expand", _dev.ptr(seeds), 1024, 3, _dev.ptr(out),
           ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
 prg.mask_stream(bytes(range(16)), 3, 1001, 32)
 xs = share(encode_fixed(rng.uniform(-10, 10, (2, 8, 8)), 3, 32), rng, precision=3)

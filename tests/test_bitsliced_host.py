@@ -1,4 +1,4 @@
-"""CPU check of the bitsliced AES circuit (csrc/aes_bitsliced.cuh, the measured
+"""CPU check of the bitsliced AES circuit (scripts/research/bitsliced/aes_bitsliced.cuh, the measured
 alternative to the T-table AES): the same header is compiled for the host with
 g++ and must reproduce the reference's PRG vectors and the oracle's expand
 bit-exactly."""
@@ -13,7 +13,8 @@ import pytest
 
 from conftest import GOLDEN, ROOT
 
-CSRC = os.path.join(ROOT, "paper_2006_04593_b200", "csrc")
+CSRC = os.path.join(ROOT, "paper_2006_04593_b200", "csrc")          # aes_consts.h
+BSDIR = os.path.join(ROOT, "scripts", "research", "bitsliced")     # aes_bitsliced.cuh
 
 
 @pytest.fixture(scope="module")
@@ -21,7 +22,7 @@ def exe(tmp_path_factory):
     if shutil.which("g++") is None:
         pytest.skip("g++ not available")
     out = str(tmp_path_factory.mktemp("bs") / "bitsliced_host")
-    subprocess.run(["g++", "-O2", "-std=c++17", "-I", CSRC,
+    subprocess.run(["g++", "-O2", "-std=c++17", "-I", BSDIR, "-I", CSRC,
                     os.path.join(ROOT, "tests", "native", "bitsliced_host.cpp"), "-o", out],
                    check=True)
     return out

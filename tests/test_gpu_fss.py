@@ -315,10 +315,19 @@ def test_host_paths_match_device_path():
 
 
 def test_bitsliced_expand_matches_ttable():
-    # the bitsliced AES alternative (csrc/aes_bitsliced.cuh) is bit-exact with the
-    # T-table PRG and the reference's PRG vectors
+    # the bitsliced AES alternative (research record, scripts/research/bitsliced,
+    # not in the product library) is bit-exact with the T-table PRG and the
+    # reference's PRG vectors
     import ctypes
-    from paper_2006_04593_b200 import _dev, _lib
+    import importlib.util
+    from paper_2006_04593_b200 import _dev
+    spec = importlib.util.spec_from_file_location(
+        "bs_build", os.path.join(os.path.dirname(GOLDEN), "..", "scripts", "research", "bitsliced", "build.py"))
+    bs_build = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bs_build)
+    bs = ctypes.CDLL(bs_build.build())
+    bs.fss_aes_mmo_expand_bitsliced.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int,
+                                                ctypes.c_void_p, ctypes.c_void_p]
     seeds = torch.from_numpy(np.random.default_rng(41).integers(0, 256, (1 << 16, 16),
                                                                 dtype=np.uint8)).cuda()
     with open(os.path.join(GOLDEN, "prg_vectors.json")) as fh:
@@ -327,8 +336,8 @@ def test_bitsliced_expand_matches_ttable():
         seeds[i] = torch.from_numpy(np.frombuffer(bytes.fromhex(s), dtype=np.uint8).copy())
     for blocks in (2, 3):
         out = torch.empty((seeds.shape[0], 16 * blocks), dtype=torch.uint8, device="cuda")
-        _lib.call("fss_aes_mmo_expand_bitsliced", _dev.ptr(seeds), seeds.shape[0], blocks,
-                  _dev.ptr(out), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        assert bs.fss_aes_mmo_expand_bitsliced(_dev.ptr(seeds), seeds.shape[0], blocks, _dev.ptr(out),
+                                               torch.cuda.current_stream().cuda_stream) == 0
         assert torch.equal(out, prg.expand(seeds, blocks))
     for i, (_, e) in enumerate(vecs):
         assert out[i].cpu().numpy().tobytes().hex() == e
