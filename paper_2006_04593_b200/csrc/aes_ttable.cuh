@@ -16,6 +16,7 @@
 // a per-element input bit; a per-thread mask m (0 or ~0) selects
 // rk = RK1 ^ (m & (RK1 ^ RK2)) -- one extra LOP3 per column.
 #pragma once
+#include <cuda_runtime.h>
 #include <stdint.h>
 #include "aes_consts.h"
 
@@ -49,6 +50,65 @@ __device__ __forceinline__ void fill_tables(uint32_t* tab) {
         const uint32_t v = kTe0[x];
         tab[idx] = __funnelshift_l(v, v, 8 * (2 * region + tsel));
     }
+}
+
+// The replicated tables are the same bytes for every CTA of every kernel, so
+// they are built ONCE per device into a global image (table_image_upload, at
+// the first launch on the device) and each CTA pulls its copy with four TMA
+// bulk copies (cp.async.bulk, 32 KiB each, completion on an mbarrier) instead
+// of computing 32768 words with its own threads: ~1 us from L2 whatever the
+// thread count, where the computed fill took up to tens of us for the
+// small-thread-count launches of small batches.
+#ifndef FSSB_TMA_TABLES
+#define FSSB_TMA_TABLES 1
+#endif
+static __device__ __align__(128) uint32_t g_tab_img[kTableWords];
+
+__device__ __forceinline__ void load_tables(uint32_t* tab) {
+#if FSSB_TMA_TABLES
+    __shared__ __align__(8) uint64_t bar;
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kTableBytes)
+                     : "memory");
+#pragma unroll
+        for (int c = 0; c < 4; c++)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    (uint32_t)__cvta_generic_to_shared(tab + c * (kTableWords / 4))),
+                "l"(g_tab_img + c * (kTableWords / 4)), "r"(kTableBytes / 4), "r"(b)
+                : "memory");
+    }
+    __syncthreads();   // the barrier is initialised before anyone waits on it
+    asm volatile(
+        "{\n .reg .pred p;\n TAB_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        " @!p bra TAB_WAIT_%=;\n}" ::"r"(b)
+        : "memory");
+#else
+    fill_tables(tab);
+    __syncthreads();
+#endif
+}
+
+// Host side: build the image from kTe0 and upload it to the current device
+// (synchronous; once per device, before the first table-using launch).
+inline cudaError_t table_image_upload() {
+    static thread_local uint32_t te0[256];
+    cudaError_t err = cudaMemcpyFromSymbol(te0, kTe0, sizeof(te0));
+    if (err != cudaSuccess) return err;
+    uint32_t* img = new uint32_t[kTableWords];
+    for (int idx = 0; idx < kTableWords; idx++) {
+        const int tsel = (idx >> 5) & 1, x = (idx >> 6) & 255, region = idx >> 14;
+        const uint32_t v = te0[x];
+        const int r = 8 * (2 * region + tsel);
+        img[idx] = r ? (v << r) | (v >> (32 - r)) : v;
+    }
+    err = cudaMemcpyToSymbol(g_tab_img, img, sizeof(uint32_t) * kTableWords);
+    delete[] img;
+    return err;
 }
 
 struct Tab {
@@ -190,42 +250,6 @@ __device__ __forceinline__ void mmo_half(const Tab& tb, U4 s, uint32_t hm, uint3
     const uint32_t s_lo = hm ? s.z : s.x, s_hi = hm ? s.w : s.y;
     lo = lop3_xor3(last_col(tb, a0, a1, a2, a3), k_lo, s_lo);
     hi = lop3_xor3(last_col(tb, a1, a2, a3, a0), k_hi, s_hi);
-}
-
-// ---- per-lane key among all three fixed keys (lane-pair evaluation) ----
-// rk = RK1 ^ (ma & (RK1 ^ RK2)) ^ (mb & (RK1 ^ RK3)): ma selects k2, mb selects
-// k3 (never both). Lanes of one warp then run ONE instruction stream while
-// encrypting under different keys -- one more LOP3 per column than SEL.
-__device__ __forceinline__ uint32_t rk3(int w, uint32_t ma, uint32_t mb) {
-    return lop3_xor_and(lop3_xor_and(kRK[0][w], ma, kRK[0][w] ^ kRK[1][w]), mb, kRK[0][w] ^ kRK[2][w]);
-}
-
-__device__ __forceinline__ U4 mmo3(const Tab& tb, U4 s, uint32_t ma, uint32_t mb) {
-    uint32_t c0 = s.x ^ rk3(0, ma, mb), c1 = s.y ^ rk3(1, ma, mb);
-    uint32_t c2 = s.z ^ rk3(2, ma, mb), c3 = s.w ^ rk3(3, ma, mb);
-#pragma unroll
-    for (int r = 1; r < 10; r++) {
-#define FSSB_MIX3(A, B, C, D, W)                                                                   \
-    lop3_xor_and(lop3_xor_and(lop3_xor3(lop3_xor3(T<0, 0>(tb, A), T<1, 1>(tb, B), T<2, 2>(tb, C)),  \
-                                        T<3, 3>(tb, D), kRK[0][W]),                                 \
-                              ma, kRK[0][W] ^ kRK[1][W]),                                           \
-                 mb, kRK[0][W] ^ kRK[2][W])
-        const uint32_t n0 = FSSB_MIX3(c0, c1, c2, c3, 4 * r + 0);
-        const uint32_t n1 = FSSB_MIX3(c1, c2, c3, c0, 4 * r + 1);
-        const uint32_t n2 = FSSB_MIX3(c2, c3, c0, c1, 4 * r + 2);
-        const uint32_t n3 = FSSB_MIX3(c3, c0, c1, c2, 4 * r + 3);
-#undef FSSB_MIX3
-        c0 = n0;
-        c1 = n1;
-        c2 = n2;
-        c3 = n3;
-    }
-    U4 o;
-    o.x = lop3_xor3(last_col(tb, c0, c1, c2, c3), rk3(40, ma, mb), s.x);
-    o.y = lop3_xor3(last_col(tb, c1, c2, c3, c0), rk3(41, ma, mb), s.y);
-    o.z = lop3_xor3(last_col(tb, c2, c3, c0, c1), rk3(42, ma, mb), s.z);
-    o.w = lop3_xor3(last_col(tb, c3, c0, c1, c2), rk3(43, ma, mb), s.w);
-    return o;
 }
 
 // Matyas-Meyer-Oseas block: AES_k(s) XOR s  (reference prg.expand, prg.py:43-60).

@@ -54,14 +54,15 @@ namespace {
 #ifndef FSSB_THREADS
 #define FSSB_THREADS 1024
 #endif
-// Batches of at most this many elements per SM use the lane-pair DCF eval
-// kernel (0 disables it).
-#ifndef FSSB_PAIR_MAX_PER_SM
-#define FSSB_PAIR_MAX_PER_SM 0
+// Keygen through the lane-pair kernel (keygen_pair_kernel): DCF at every
+// size (1024 threads x 64 registers beat 512 x 128 even at 2^22: -0.7 %, and
+// -12 % at 2^16), DPF not (+2.4 % at 2^22; scripts/small_batch_probe.py,
+// profiles/r02_small_batch.json).
+#ifndef FSSB_KEYGEN_PAIR_DCF
+#define FSSB_KEYGEN_PAIR_DCF 1
 #endif
-// ... and of keygen (lane-pair keygen kernel; 0 disables it)
-#ifndef FSSB_KEYGEN_PAIR_MAX_PER_SM
-#define FSSB_KEYGEN_PAIR_MAX_PER_SM 0
+#ifndef FSSB_KEYGEN_PAIR_DPF
+#define FSSB_KEYGEN_PAIR_DPF 0
 #endif
 // Eval kernels: 32 warps per SM (64 registers) hide the LDS / LDG latency best
 // (profiles/r01_aes_variants_b.json: 512 -> 1024 threads = +5 % DCF, +17 % DPF).
@@ -110,9 +111,8 @@ __device__ __forceinline__ Span cta_span(uint64_t count) {
 // prg.expand (prg.py:43-60): out block b = AES_{k_b}(seed) ^ seed.
 __global__ void __launch_bounds__(kKeygenThreads, 1)
 expand_kernel(const uint8_t* __restrict__ seeds, uint64_t count, int blocks, uint8_t* __restrict__ out) {
-    extern __shared__ uint32_t tab[];
-    fssb::fill_tables(tab);
-    __syncthreads();
+    extern __shared__ __align__(128) uint32_t tab[];
+    fssb::load_tables(tab);
     const fssb::Tab tb = fssb::make_tab(tab);
     const Span sp = cta_span(count);
     for (uint64_t e = sp.lo + threadIdx.x; e < sp.hi; e += blockDim.x) {
@@ -142,9 +142,8 @@ __device__ __forceinline__ uint64_t load_x(const uint64_t* __restrict__ x, const
 __global__ void __launch_bounds__(kKeygenThreads, 1)
 mask_stream_kernel(U4 seed, uint64_t round_idx, uint64_t blocks, uint64_t count, uint64_t mask,
                    uint64_t* __restrict__ out) {
-    extern __shared__ uint32_t tab[];
-    fssb::fill_tables(tab);
-    __syncthreads();
+    extern __shared__ __align__(128) uint32_t tab[];
+    fssb::load_tables(tab);
     const fssb::Tab tb = fssb::make_tab(tab);
     const Span sp = cta_span(blocks);
     for (uint64_t i = sp.lo + threadIdx.x; i < sp.hi; i += blockDim.x) {
@@ -162,15 +161,16 @@ mask_stream_kernel(U4 seed, uint64_t round_idx, uint64_t blocks, uint64_t count,
 // ---------------------------------------------------------------- DPF eval
 // fss.eval_eq (fss.py:357-377): t0 = party, per level expand, correct with
 // scw/tcw when t, descend to child x_i (MSB first); out = t*cw_final + s2r(s).
+//
 __global__ void __launch_bounds__(kThreads, 1)
 dpf_eval_kernel(int party, int n, uint64_t count, uint64_t ld, const uint8_t* __restrict__ seed0,
                 const uint8_t* __restrict__ scw, const uint8_t* __restrict__ tcw,
                 const uint64_t* __restrict__ cw_final, const uint64_t* __restrict__ x,
                 const void* __restrict__ m_own, const void* __restrict__ m_peer,
                 uint64_t* __restrict__ out) {
-    extern __shared__ uint32_t tab[];
-    fssb::fill_tables(tab);
-    __syncthreads();
+    constexpr bool PF = FSSB_PREFETCH_DPF;
+    extern __shared__ __align__(128) uint32_t tab[];
+    fssb::load_tables(tab);
     const fssb::Tab tb = fssb::make_tab(tab);
     const uint64_t mask = ring_mask(n);
     const Span sp = cta_span(count);
@@ -178,21 +178,21 @@ dpf_eval_kernel(int party, int n, uint64_t count, uint64_t ld, const uint8_t* __
         U4 s = ld16(seed0 + 16 * e);
         uint32_t t = party;
         const uint64_t xe = load_x(x, m_own, m_peer, n, e) & mask;
-#if FSSB_PREFETCH_DPF
         // software pipeline: level i+1's correction words load during level i's AES
-        U4 cw = ld16(scw + 16 * e);
-        uint32_t f = __ldg(tcw + e);
-#endif
+        U4 cw = PF ? ld16(scw + 16 * e) : U4{0, 0, 0, 0};
+        uint32_t f = PF ? __ldg(tcw + e) : 0u;
         for (int i = 0; i < n; i++) {
-#if FSSB_PREFETCH_DPF
-            const uint64_t offn = (uint64_t)(i + 1 < n ? i + 1 : i) * ld + e;
-            const U4 cw_next = ld16(scw + 16 * offn);
-            const uint32_t f_next = __ldg(tcw + offn);
-#else
-            const uint64_t off = (uint64_t)i * ld + e;
-            const U4 cw = ld16(scw + 16 * off);
-            const uint32_t f = __ldg(tcw + off);
-#endif
+            U4 cw_next;
+            uint32_t f_next;
+            if (PF) {
+                const uint64_t offn = (uint64_t)(i + 1 < n ? i + 1 : i) * ld + e;
+                cw_next = ld16(scw + 16 * offn);
+                f_next = __ldg(tcw + offn);
+            } else {
+                const uint64_t off = (uint64_t)i * ld + e;
+                cw = ld16(scw + 16 * off);
+                f = __ldg(tcw + off);
+            }
             const uint32_t xb = (uint32_t)(xe >> (n - 1 - i)) & 1u;
             const U4 a = fssb::mmo<0, true>(tb, s, 0u - xb);
             const uint32_t tm = 0u - t;
@@ -200,10 +200,10 @@ dpf_eval_kernel(int party, int n, uint64_t count, uint64_t ld, const uint8_t* __
             const uint32_t tn = ((a.w >> 31) ^ (t & (f >> xb))) & 1u;
             s.w &= 0x7FFFFFFFu;
             t = tn;
-#if FSSB_PREFETCH_DPF
-            cw = cw_next;
-            f = f_next;
-#endif
+            if (PF) {
+                cw = cw_next;
+                f = f_next;
+            }
         }
         uint64_t o = (((uint64_t)t * cw_final[e]) + lo64(s)) & mask;
         if (party) o = (0 - o) & mask;
@@ -233,9 +233,8 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
                 const void* __restrict__ m_own, const void* __restrict__ m_peer,
                 uint64_t* __restrict__ out, uint64_t* __restrict__ levels) {
     using W = typename std::conditional<W32, uint32_t, uint64_t>::type;
-    extern __shared__ uint32_t tab[];
-    fssb::fill_tables(tab);
-    __syncthreads();
+    extern __shared__ __align__(128) uint32_t tab[];
+    fssb::load_tables(tab);
     const fssb::Tab tb = fssb::make_tab(tab);
     const uint64_t nmask = ring_mask(n);
     const uint64_t mask = ring_mask(out_bits);
@@ -270,11 +269,11 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
             const W leaf = __ldg(leaf_w + kStride * off);
 #endif
             const uint32_t xb = (uint32_t)(xe >> (n - 1 - i)) & 1u;
-            const U4 a = fssb::mmo<0, true>(tb, s, 0u - xb);
             const uint32_t tm = 0u - t;
             // sigma/tau lane x_i of the third block (slice_cmp, prg.py:99-119):
             // only that 8-byte half of AES_k3(s) ^ s is computed
             uint32_t lane_lo, lane_hi;
+            const U4 a = fssb::mmo<0, true>(tb, s, 0u - xb);
             fssb::mmo_half<2>(tb, s, 0u - xb, lane_lo, lane_hi);
             W lane;
             if (W32) lane = (W)lane_lo;
@@ -301,77 +300,6 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
         acc += last;
         if (LEVELS) levels[(uint64_t)n * count + e] = (party ? (0 - (uint64_t)last) : (uint64_t)last) & mask;
         out[e] = (party ? (0 - (uint64_t)acc) : (uint64_t)acc) & mask;
-    }
-}
-
-// ------------------------------------------------- DCF eval, lane pairs
-// Small batches (config 1: 2^16 keys = 443 per SM) leave the one-lane kernel
-// with too few warps per SM to keep the LDS pipe busy. Here a PAIR of lanes
-// evaluates one element: the even lane encrypts the child block (key k1/k2 by
-// x_i), the odd lane the sigma/tau block (k3) -- one instruction stream with a
-// per-lane key (mmo3) -- and the even lane's child block is shuffled to its
-// partner, so both lanes carry the same (s, t) down the tree. The odd lane
-// accumulates and stores the output. Per level 2 x 160 lookups (+8 over the
-// half-block trick) and 4 SHFL, for twice the warps per element.
-template <bool W32>
-__global__ void __launch_bounds__(kThreads, 1)
-dcf_eval_pair_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
-                     const uint8_t* __restrict__ seed0, const uint8_t* __restrict__ scw,
-                     const uint8_t* __restrict__ tcw, const uint64_t* __restrict__ sigma_cw,
-                     const uint64_t* __restrict__ leaf_cw, const uint64_t* __restrict__ x,
-                     const void* __restrict__ m_own, const void* __restrict__ m_peer,
-                     uint64_t* __restrict__ out) {
-    using W = typename std::conditional<W32, uint32_t, uint64_t>::type;
-    extern __shared__ uint32_t tab[];
-    fssb::fill_tables(tab);
-    __syncthreads();
-    const fssb::Tab tb = fssb::make_tab(tab);
-    const uint64_t nmask = ring_mask(n);
-    const uint64_t mask = ring_mask(out_bits);
-    const W* __restrict__ sig_w = reinterpret_cast<const W*>(sigma_cw);
-    const W* __restrict__ leaf_w = reinterpret_cast<const W*>(leaf_cw);
-    constexpr int kStride = W32 ? 2 : 1;
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t odd = lane & 1;
-    const uint32_t pm = 3u << (lane & ~1u);       // the pair's shuffle mask
-    const uint32_t mb = 0u - odd;                  // odd lane: key k3
-    const Span sp = cta_span(count);
-    for (uint64_t e = sp.lo + (threadIdx.x >> 1); e < sp.hi; e += blockDim.x >> 1) {
-        U4 s = ld16(seed0 + 16 * e);
-        uint32_t t = party;
-        W acc = 0;
-        const uint64_t xe = load_x(x, m_own, m_peer, n, e) & nmask;
-        for (int i = 0; i < n; i++) {
-            const uint64_t off = (uint64_t)i * ld + e;
-            const U4 cw = ld16(scw + 16 * off);
-            const uint32_t f = __ldg(tcw + off);
-            const uint32_t xb = (uint32_t)(xe >> (n - 1 - i)) & 1u;
-            const U4 b = fssb::mmo3(tb, s, (0u - xb) & ~mb, mb);
-            U4 a;
-            a.x = __shfl_sync(pm, b.x, lane & ~1u);
-            a.y = __shfl_sync(pm, b.y, lane & ~1u);
-            a.z = __shfl_sync(pm, b.z, lane & ~1u);
-            a.w = __shfl_sync(pm, b.w, lane & ~1u);
-            if (odd) {   // sigma/tau lane x_i of the third block (slice_cmp, prg.py:99-119)
-                const W sig = __ldg(sig_w + kStride * off);
-                const W leaf = __ldg(leaf_w + kStride * off);
-                const uint32_t lane_lo = xb ? b.z : b.x, lane_hi = xb ? b.w : b.y;
-                const W lv = W32 ? (W)lane_lo : (W)(((uint64_t)lane_hi << 32) | lane_lo);
-                const uint32_t tau = ((lane_hi >> 31) ^ (t & (f >> (2 + xb)))) & 1u;
-                const W sigma = lv ^ (sig & (W)(0 - (W)t));
-                acc += (leaf & (W)(0 - (W)tau)) + sigma;
-            }
-            s = xor4(a, and4(cw, 0u - t));
-            const uint32_t tn = ((a.w >> 31) ^ (t & (f >> xb))) & 1u;
-            s.w &= 0x7FFFFFFFu;
-            t = tn;
-        }
-        if (odd) {
-            const uint64_t off = (uint64_t)n * ld + e;
-            const W lo = W32 ? (W)s.x : (W)lo64(s);
-            acc += (__ldg(leaf_w + kStride * off) & (W)(0 - (W)t)) + lo;
-            out[e] = (party ? (0 - (uint64_t)acc) : (uint64_t)acc) & mask;
-        }
     }
 }
 
@@ -439,9 +367,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 dcf_eval_packed_kernel(int party, int n, uint64_t count, const uint8_t* __restrict__ payload,
                        const uint64_t* __restrict__ x, const void* __restrict__ m_own,
                        const void* __restrict__ m_peer, uint64_t* __restrict__ out) {
-    extern __shared__ uint32_t tab[];
-    fssb::fill_tables(tab);
-    __syncthreads();
+    extern __shared__ __align__(128) uint32_t tab[];
+    fssb::load_tables(tab);
     const fssb::Tab tb = fssb::make_tab(tab);
     constexpr uint32_t rec = 17 + W;
     constexpr int NW = (17 + W + 3) / 4;          // words of one level record
@@ -490,9 +417,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 dpf_eval_packed_kernel(int party, int n, uint64_t count, const uint8_t* __restrict__ payload,
                        const uint64_t* __restrict__ x, const void* __restrict__ m_own,
                        const void* __restrict__ m_peer, uint64_t* __restrict__ out) {
-    extern __shared__ uint32_t tab[];
-    fssb::fill_tables(tab);
-    __syncthreads();
+    extern __shared__ __align__(128) uint32_t tab[];
+    fssb::load_tables(tab);
     const fssb::Tab tb = fssb::make_tab(tab);
     const uint64_t EB = W + 16 + 17 * (uint64_t)n + W;
     const uint64_t mask = ring_mask(n);
@@ -531,9 +457,8 @@ dpf_keygen_kernel(int n, uint64_t count, const uint64_t* __restrict__ alpha,
                   const uint8_t* __restrict__ s1_init, uint8_t* __restrict__ scw,
                   uint8_t* __restrict__ tcw, uint64_t* __restrict__ cw_final,
                   uint64_t* __restrict__ alpha1) {
-    extern __shared__ uint32_t tab[];
-    fssb::fill_tables(tab);
-    __syncthreads();
+    extern __shared__ __align__(128) uint32_t tab[];
+    fssb::load_tables(tab);
     const fssb::Tab tb = fssb::make_tab(tab);
     const uint64_t mask = ring_mask(n);
     const Span sp = cta_span(count);
@@ -576,9 +501,8 @@ dcf_keygen_kernel(int n, int out_bits, uint64_t count, const uint64_t* __restric
                   const uint8_t* __restrict__ s1_init, uint8_t* __restrict__ scw,
                   uint8_t* __restrict__ tcw, uint64_t* __restrict__ sigma_cw,
                   uint64_t* __restrict__ leaf_cw, uint64_t* __restrict__ alpha1) {
-    extern __shared__ uint32_t tab[];
-    fssb::fill_tables(tab);
-    __syncthreads();
+    extern __shared__ __align__(128) uint32_t tab[];
+    fssb::load_tables(tab);
     const fssb::Tab tb = fssb::make_tab(tab);
     const uint64_t nmask = ring_mask(n);
     const uint64_t mask = ring_mask(out_bits);
@@ -648,9 +572,8 @@ keygen_pair_kernel(int n, int out_bits, uint64_t count, const uint64_t* __restri
                    uint8_t* __restrict__ tcw, uint64_t* __restrict__ sigma_cw,
                    uint64_t* __restrict__ leaf_cw, uint64_t* __restrict__ cw_final,
                    uint64_t* __restrict__ alpha1) {
-    extern __shared__ uint32_t tab[];
-    fssb::fill_tables(tab);
-    __syncthreads();
+    extern __shared__ __align__(128) uint32_t tab[];
+    fssb::load_tables(tab);
     const fssb::Tab tb = fssb::make_tab(tab);
     const uint64_t nmask = ring_mask(n);
     const uint64_t mask = ring_mask(out_bits);
@@ -946,6 +869,11 @@ int prep_launch(K kernel, int* grid) {
     if (!d.sms) {
         err = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
         if (err != cudaSuccess) return set_err(kEcuda, "cudaDeviceGetAttribute: %s", cudaGetErrorString(err));
+        err = fssb::table_image_upload();   // the T-table image the kernels' TMA copies read
+        if (err != cudaSuccess) {
+            d.sms = 0;
+            return set_err(kEcuda, "T-table image upload: %s", cudaGetErrorString(err));
+        }
     }
     bool done = false;
     for (const void* k : d.attr_done) done |= (k == key);
@@ -1048,18 +976,6 @@ int launch_dcf_eval(int party, int n, int out_bits, uint64_t count, uint64_t ld,
     FSS_REQUIRE(seed0, scw, tcw, sigma_cw, leaf_cw, out);
     int sms;
     const bool w32 = FSSB_W32 && out_bits <= 32;
-    if (!levels && FSSB_PAIR_MAX_PER_SM > 0) {
-        // small batch: two lanes per element (dcf_eval_pair_kernel)
-        auto pk = w32 ? dcf_eval_pair_kernel<true> : dcf_eval_pair_kernel<false>;
-        if (int rc = prep_launch(pk, &sms)) return rc;
-        if (count <= (uint64_t)sms * FSSB_PAIR_MAX_PER_SM) {
-            int threads;
-            const int grid = balanced_grid(2 * count, sms, kThreads, &threads);
-            pk<<<grid, threads, fssb::kTableBytes, (cudaStream_t)stream>>>(
-                party, n, out_bits, count, ld, seed0, scw, tcw, sigma_cw, leaf_cw, x, m_own, m_peer, out);
-            return check_launch();
-        }
-    }
     auto kern = levels ? (w32 ? dcf_eval_kernel<true, true> : dcf_eval_kernel<false, true>)
                        : (w32 ? dcf_eval_kernel<true, false> : dcf_eval_kernel<false, false>);
     if (int rc = prep_launch(kern, &sms)) return rc;
@@ -1313,9 +1229,9 @@ int fss_dpf_keygen(int n, uint64_t count, const uint64_t* alpha, const uint64_t*
     if (count == 0) return kOk;
     FSS_REQUIRE(alpha, alpha0, s0, s1, scw, tcw, cw_final, alpha1);
     int sms;
-    if (FSSB_KEYGEN_PAIR_MAX_PER_SM > 0) {
+    if (FSSB_KEYGEN_PAIR_DPF) {
         if (int rc = prep_launch(keygen_pair_kernel<false>, &sms)) return rc;
-        if (count <= (uint64_t)sms * FSSB_KEYGEN_PAIR_MAX_PER_SM) {
+        {
             int threads;
             const int grid = balanced_grid(2 * count, sms, kPairKeygenThreads, &threads);
             keygen_pair_kernel<false><<<grid, threads, fssb::kTableBytes, (cudaStream_t)stream>>>(
@@ -1340,9 +1256,9 @@ int fss_dcf_keygen(int n, int out_bits, uint64_t count, const uint64_t* alpha,
     if (count == 0) return kOk;
     FSS_REQUIRE(alpha, alpha0, s0, s1, scw, tcw, sigma_cw, leaf_cw, alpha1);
     int sms;
-    if (FSSB_KEYGEN_PAIR_MAX_PER_SM > 0) {
+    if (FSSB_KEYGEN_PAIR_DCF) {
         if (int rc = prep_launch(keygen_pair_kernel<true>, &sms)) return rc;
-        if (count <= (uint64_t)sms * FSSB_KEYGEN_PAIR_MAX_PER_SM) {
+        {
             int threads;
             const int grid = balanced_grid(2 * count, sms, kPairKeygenThreads, &threads);
             keygen_pair_kernel<true><<<grid, threads, fssb::kTableBytes, (cudaStream_t)stream>>>(

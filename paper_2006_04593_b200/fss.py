@@ -147,11 +147,12 @@ class EqKeyBatch:
             raise KeyFormatError("seed/final arrays do not match count")
         _check_party_tensors(self, ("seed0", "scw", "tcw", "cw_final"))
 
-    def take(self, idx) -> "EqKeyBatch":
+    def take(self, idx, _consumed=None) -> "EqKeyBatch":
         sel, arr = _index(idx, self.count, self.device)
         return EqKeyBatch(self.party, self.n_bits, _take1(self.alpha_share, sel),
                           _take1(self.seed0, sel), _take2(self.scw, sel), _take2(self.tcw, sel),
-                          _take1(self.cw_final, sel), self.consumed[arr].copy())
+                          _take1(self.cw_final, sel),
+                          self.consumed[arr].copy() if _consumed is None else _consumed)
 
     def take_unused(self, m: int) -> "EqKeyBatch":
         return _take_unused(self, m)
@@ -196,12 +197,12 @@ class CmpKeyBatch:
             raise KeyFormatError("seed array does not match count")
         _check_party_tensors(self, ("seed0", "scw", "tcw", "sigma_cw", "leaf_cw"))
 
-    def take(self, idx) -> "CmpKeyBatch":
+    def take(self, idx, _consumed=None) -> "CmpKeyBatch":
         sel, arr = _index(idx, self.count, self.device)
         return CmpKeyBatch(self.party, self.n_bits, _take1(self.alpha_share, sel),
                            _take1(self.seed0, sel), _take2(self.scw, sel), _take2(self.tcw, sel),
                            _take2(self.sigma_cw, sel), _take2(self.leaf_cw, sel),
-                           self.consumed[arr].copy(), self.out_bits)
+                           self.consumed[arr].copy() if _consumed is None else _consumed, self.out_bits)
 
     def take_unused(self, m: int) -> "CmpKeyBatch":
         return _take_unused(self, m)
@@ -261,10 +262,10 @@ class PackedKeyBatch:
         if not self.payload.is_contiguous():
             raise KeyFormatError("payload rows must be contiguous")
 
-    def take(self, idx) -> "PackedKeyBatch":
+    def take(self, idx, _consumed=None) -> "PackedKeyBatch":
         sel, arr = _index(idx, self.count, self.device)
         return PackedKeyBatch(self.kind, self.party, self.n_bits, _take1(self.payload, sel),
-                              self.consumed[arr].copy())
+                              self.consumed[arr].copy() if _consumed is None else _consumed)
 
     def take_unused(self, m: int) -> "PackedKeyBatch":
         return _take_unused(self, m)
@@ -298,32 +299,47 @@ def _eval_packed(party: int, k: PackedKeyBatch, x, out, m_own=None, m_peer=None)
     return _run_eval(launch, xt, host, count, dev, None, out)
 
 
+_SPENT = np.ones(0, dtype=bool)
+
+
+def _spent(m: int) -> np.ndarray:
+    """A read-only all-True mask of m keys: the ``consumed`` field of a batch
+    handed out by take_unused (every key of it is spent). One shared buffer,
+    so a hand-out of millions of keys costs no mask allocation or copy."""
+    global _SPENT
+    if _SPENT.shape[0] < m:
+        buf = np.ones(max(m, 2 * _SPENT.shape[0]), dtype=bool)
+        buf.setflags(write=False)
+        _SPENT = buf
+    return _SPENT[:m]
+
+
 def _take_unused(batch, m: int):
     """Single-use key hand-out (fss.py:157-166): the first m unconsumed keys.
 
     Keys are normally spent front to back. ``_free_hint`` h keeps the invariant
     consumed[:h] all True (consuming more keys never breaks it), so when
     consumed[h : h+m] are all free they ARE the first m free keys and go out as
-    one contiguous zero-copy slice in O(m); otherwise the full scan is used."""
+    one contiguous zero-copy slice in O(m); otherwise the full scan is used.
+    The handed-out batch is spent: its mask is a read-only all-True view."""
     consumed = batch.consumed
     count = consumed.shape[0]
     h = min(getattr(batch, "_free_hint", 0), count)
     if h and not consumed[h - 1]:   # mask was replaced / edited: drop the hint
         h = 0
     if m == 0 or (h + m <= count and not consumed[h:h + m].any()):
-        out = batch.take(slice(h, h + m))
-        consumed[h:h + m] = True
+        out = batch.take(slice(h, h + m), _consumed=_spent(m))
+        if m:
+            consumed[h:h + m] = True
         batch._free_hint = h + m
-        out.consumed[:] = True
         return out
     free = np.flatnonzero(~consumed)
     if free.size < m:
         raise KeyExhaustedError(
             f"requested {m} keys but only {free.size} unconsumed remain (single-use)")
     idx = free[:m]
-    out = batch.take(idx)
+    out = batch.take(idx, _consumed=_spent(m))   # the view itself is spent once handed out
     consumed[idx] = True
-    out.consumed[:] = True  # the view itself is spent once handed out
     # everything before the next free key is now consumed
     batch._free_hint = int(free[m]) if free.size > m else count
     return out

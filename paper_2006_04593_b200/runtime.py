@@ -487,16 +487,59 @@ def _party_streams(dev) -> list:
     return _PARTY_STREAMS[key]
 
 
+class _PartyWorkers:
+    """Two long-lived party threads (one per party), reused by every
+    run_local_pair call: starting two fresh threads per online run costs more
+    host time than a small protocol's kernels (config 1: 2^16 comparisons).
+    A job is a callable; the worker runs it and reports (result, error)."""
+
+    def __init__(self):
+        self._jobs = [queue.SimpleQueue(), queue.SimpleQueue()]
+        self._done = [queue.SimpleQueue(), queue.SimpleQueue()]
+        self.lock = threading.Lock()
+        self.threads = [threading.Thread(target=self._loop, args=(p,), daemon=True,
+                                         name=f"ariann-party{p}") for p in (0, 1)]
+        for t in self.threads:
+            t.start()
+
+    def _loop(self, party):
+        while True:
+            job = self._jobs[party].get()
+            try:
+                self._done[party].put((job(), None))
+            except BaseException as exc:  # noqa: BLE001 -- handed to the caller
+                self._done[party].put((None, exc))
+
+    def run(self, job0, job1):
+        self._jobs[0].put(job0)
+        self._jobs[1].put(job1)
+        return self._done[0].get(), self._done[1].get()
+
+
+_WORKERS = None
+_WORKERS_INIT = threading.Lock()
+
+
+def _party_workers():
+    global _WORKERS
+    with _WORKERS_INIT:
+        if _WORKERS is None:
+            _WORKERS = _PartyWorkers()
+        return _WORKERS
+
+
 def run_local_pair(program0, program1=None, device=None):
     """Two programs over the in-process transport, one thread per party
     (runtime.py:285-311). Each party thread runs on its own CUDA stream of
     ``device`` so the two parties' kernels can overlap; the exchange orders
-    them. Returns ((result0, ledger0), (result1, ledger1))."""
+    them. Returns ((result0, ledger0), (result1, ledger1)).
+
+    The party threads are two persistent workers shared by all calls; a call
+    made while they are busy (another thread's run, or a nested call from
+    inside a party program) runs on two fresh threads instead."""
     if program1 is None:
         program1 = program0
     t0, t1 = local_pair()
-    results = [None, None]
-    errors = [None, None]
     dev = None
     if torch.cuda.is_available():
         dev = torch.device(device) if device is not None else torch.device(
@@ -506,28 +549,45 @@ def run_local_pair(program0, program1=None, device=None):
         for s in streams:
             s.wait_stream(parent)
 
-    def runner(party, transport, program):
-        try:
-            if dev is not None:
-                with torch.cuda.device(dev), torch.cuda.stream(streams[party]):
-                    results[party] = run_session(party, transport, program)
-            else:
-                results[party] = run_session(party, transport, program)
-        except BaseException as exc:  # propagate to the caller
-            errors[party] = exc
-            transport.close()
+    def job(party, transport, program):
+        def run():
+            try:
+                if dev is not None:
+                    with torch.cuda.device(dev), torch.cuda.stream(streams[party]):
+                        return run_session(party, transport, program)
+                return run_session(party, transport, program)
+            except BaseException:
+                transport.close()       # unblock the peer
+                raise
+        return run
 
-    th0 = threading.Thread(target=runner, args=(0, t0, program0))
-    th1 = threading.Thread(target=runner, args=(1, t1, program1))
-    th0.start(); th1.start()
-    th0.join(); th1.join()
+    jobs = (job(0, t0, program0), job(1, t1, program1))
+    workers = _party_workers()
+    if workers.lock.acquire(blocking=False):
+        try:
+            outcome = workers.run(*jobs)
+        finally:
+            workers.lock.release()
+    else:
+        outcome = [[None, None], [None, None]]
+
+        def fresh(p):
+            try:
+                outcome[p][0] = jobs[p]()
+            except BaseException as exc:  # noqa: BLE001
+                outcome[p][1] = exc
+        ths = [threading.Thread(target=fresh, args=(p,)) for p in (0, 1)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
     if dev is not None:
         for s in streams:
             parent.wait_stream(s)
-    for err in errors:
+    for _, err in outcome:
         if err is not None:
             raise err
-    return results[0], results[1]
+    return outcome[0][0], outcome[1][0]
 
 
 def run_dist_party(party: int, peer: int, program, group=None, device=None):

@@ -1,0 +1,103 @@
+"""Host-side timeline of one in-process two-party online run (no profiler):
+wraps the protocol's host entry points with perf_counter spans per party
+thread and prints them relative to the run start, plus the wall time.
+
+  python scripts/host_timeline.py [relu|config1|argmax]
+"""
+import functools
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2006_04593_b200 import beaver, dealer, fss, nn_ops, runtime, sharing  # noqa: E402
+from paper_2006_04593_b200.sharing import AdditiveShare, encode_fixed, share  # noqa: E402
+
+what = sys.argv[1] if len(sys.argv) > 1 else "relu"
+LOG = []
+
+
+def wrap(mod, name, label=None):
+    fn = getattr(mod, name)
+
+    @functools.wraps(fn)
+    def w(*a, **k):
+        t0 = time.perf_counter()
+        try:
+            return fn(*a, **k)
+        finally:
+            LOG.append((threading.current_thread().name, label or name, t0, time.perf_counter()))
+    setattr(mod, name, w)
+
+
+for mod, names in ((fss, ["sign_protocol", "eq_protocol", "_masked_round", "_eval_cmp_masked",
+                          "_eval_eq_masked"]),
+                   (beaver, ["beaver_protocol"]), (nn_ops, ["relu", "argmax", "maxpool"])):
+    for n in names:
+        wrap(mod, n, f"{mod.__name__.split('.')[-1]}.{n}")
+_orig_ex = runtime.Session.exchange
+
+
+def _ex(self, *a, **k):
+    t0 = time.perf_counter()
+    try:
+        return _orig_ex(self, *a, **k)
+    finally:
+        LOG.append((threading.current_thread().name, "exchange", t0, time.perf_counter()))
+
+
+runtime.Session.exchange = _ex
+rng = np.random.default_rng(4)
+if what == "relu":
+    shape = (1, 64, 112, 112)
+    xs = share(encode_fixed(rng.uniform(-100, 100, shape), 3, 32), rng, precision=3)
+elif what == "config1":
+    xs = share(encode_fixed(rng.uniform(-100, 100, 1 << 16), 3, 32), rng, precision=3)
+else:
+    xs = share(encode_fixed(rng.uniform(-10, 10, (16, 64, 56, 56)), 3, 32), rng, precision=3)
+    xs = [x.reshape(1024, 56, 56) for x in xs]
+
+
+def once():
+    d = dealer.make_dealer(32, seed=2)
+    preps = []
+    for p in (0, 1):
+        v = d.for_party(p)
+        if what == "relu":
+            preps.append(v.relu_shaped(shape))
+        elif what == "config1":
+            preps.append(v.cmp_keys(1 << 16))
+        else:
+            preps.append(v.maxpool(56, 2, 2, planes=1024))
+    torch.cuda.synchronize()
+
+    def prog(s):
+        if what == "relu":
+            return nn_ops.relu(s, xs[s.party], preps[s.party])
+        if what == "config1":
+            return fss.sign_protocol(s, AdditiveShare(s.party, xs[s.party].values, 0), preps[s.party])
+        return nn_ops.maxpool(s, xs[s.party], 2, preps[s.party], 2)
+    LOG.clear()
+    t0 = time.perf_counter()
+    runtime.run_local_pair(prog)
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    return t0, t1, t2
+
+
+for _ in range(5):
+    once()
+walls = []
+for _ in range(10):
+    t0, t1, t2 = once()
+    walls.append(t2 - t0)
+print(what, "online wall ms: median %.3f" % (sorted(walls)[5] * 1e3))
+print("last run: run_local_pair returned at %.3f ms, GPU done at %.3f ms" % ((t1 - t0) * 1e3, (t2 - t0) * 1e3))
+for th, name, a, b in sorted(LOG, key=lambda r: r[2]):
+    print("  %-12s %-28s %8.3f -> %8.3f  (%.3f ms)" % (th[-12:], name, (a - t0) * 1e3, (b - t0) * 1e3,
+                                                     (b - a) * 1e3))

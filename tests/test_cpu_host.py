@@ -143,11 +143,15 @@ def test_take_unused_fast_path_and_fallback():
             self.consumed = np.zeros(n, dtype=bool)
             self.taken = []
 
-        def take(self, idx):
+        def take(self, idx, _consumed=None):
             self.taken.append(idx)
+            # the hand-out is spent: a read-only all-True mask of its size
+            n = (idx.stop - idx.start) if isinstance(idx, slice) else len(idx)
+            assert _consumed is not None and _consumed.shape == (n,) and _consumed.all()
+            assert not _consumed.flags.writeable
 
             class V:
-                consumed = np.zeros(1, dtype=bool)
+                consumed = _consumed
             return V()
     rng = np.random.default_rng(0)
     for trial in range(200):

@@ -179,3 +179,41 @@ def test_dist_abort_mid_program_fails_fast():
     assert got[0][1] == "abort" and got[1][1] == "raised"
     assert got[0][2] < 30 and got[1][2] < 30          # not the 90 s group timeout
     assert got[0][3] == 6 and got[1][3] == 5
+
+
+def test_local_pair_reuses_workers_and_handles_nesting_and_errors():
+    import threading as th
+    names = []
+
+    def prog(session):
+        names.append(th.current_thread().name)
+        return int(session.exchange("x", runtime.FRAME_MASKED,
+                                    torch.full((2,), session.party, dtype=torch.int32), 2)[0])
+    for _ in range(3):
+        (r0, _), (r1, _) = runtime.run_local_pair(prog)
+        assert (r0, r1) == (1, 0)
+    assert set(names) == {"ariann-party0", "ariann-party1"}      # the persistent workers
+
+    def nested(session):                 # a party program that runs its own pair
+        inner = runtime.run_local_pair(prog)
+        return inner[0][0]
+    (a, _), (b, _) = runtime.run_local_pair(nested)
+    assert a == 1 and b == 1
+
+    def boom(session):
+        if session.party == 0:
+            raise KeyError("party 0 fails")
+        return session.exchange("x", runtime.FRAME_MASKED, torch.zeros(1), 1)
+    with pytest.raises((KeyError, runtime.SessionAbort)):
+        runtime.run_local_pair(boom)
+    (r0, _), (r1, _) = runtime.run_local_pair(prog)          # workers still healthy
+    assert (r0, r1) == (1, 0)
+
+    # concurrent callers: one gets the workers, the other fresh threads
+    out = []
+    ts = [th.Thread(target=lambda: out.append(runtime.run_local_pair(prog)[0][0])) for _ in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert out == [1, 1, 1, 1]
