@@ -114,6 +114,56 @@ def _check_party_tensors(k, names):
             raise KeyFormatError(f"{name} lives on {t.device}, expected {dev}")
 
 
+class _ConsumedMask:
+    """The ``consumed`` field of the key batches (reference fss.py:92-102): a
+    host numpy bool mask, as in the reference -- with the single-use hand-out
+    of ``take_unused`` kept O(1) on its common path. While a batch's mask is
+    a pure prefix (keys [0, front) spent, the rest untouched -- true of every
+    freshly generated batch spent front to back), a hand-out only records the
+    range; the recorded ranges are written into the array the next time the
+    field is read (reading also ends the fast path: the caller may edit the
+    array in place). A 9.6 M-key hand-out (config 4's argmax) thus costs no
+    0.5 ms mask scan and fill per party."""
+
+    def __get__(self, obj, objtype=None):
+        if obj is None:
+            return self
+        d = obj.__dict__
+        pend = d.get("_pend")
+        if pend:
+            arr = d["_cons"]
+            for lo, hi in pend:
+                arr[lo:hi] = True
+            pend.clear()
+        d["_front"] = None
+        return d.get("_cons")
+
+    def __set__(self, obj, value):
+        obj.__dict__.update(_cons=value, _pend=[], _front=None)
+
+    @staticmethod
+    def fresh(obj, count: int):
+        """A new all-unspent mask: the pure-prefix state with front 0."""
+        obj.__dict__.update(_cons=np.zeros(count, dtype=bool), _pend=[], _front=0)
+
+    @staticmethod
+    def take_prefix(obj, m: int):
+        """Spend [front, front + m) if the mask is a pure prefix with room;
+        returns the start of the range or None (caller takes the slow path)."""
+        d = obj.__dict__
+        front = d.get("_front")
+        if front is None or front + m > d["_cons"].shape[0]:
+            return None
+        if m:
+            pend = d["_pend"]
+            if pend and pend[-1][1] == front:
+                pend[-1] = (pend[-1][0], front + m)
+            else:
+                pend.append((front, front + m))
+        d["_front"] = front + m
+        return front
+
+
 @dataclass
 class EqKeyBatch:
     """One party's batch of equality keys (struct-of-arrays, fss.py:71-105)."""
@@ -129,7 +179,7 @@ class EqKeyBatch:
 
     def __post_init__(self):
         if self.consumed is None:
-            self.consumed = np.zeros(self.count, dtype=bool)
+            _ConsumedMask.fresh(self, self.count)
 
     @property
     def count(self) -> int:
@@ -175,7 +225,7 @@ class CmpKeyBatch:
 
     def __post_init__(self):
         if self.consumed is None:
-            self.consumed = np.zeros(self.count, dtype=bool)
+            _ConsumedMask.fresh(self, self.count)
         if self.out_bits is None:
             self.out_bits = self.n_bits
 
@@ -227,7 +277,7 @@ class PackedKeyBatch:
 
     def __post_init__(self):
         if self.consumed is None:
-            self.consumed = np.zeros(self.count, dtype=bool)
+            _ConsumedMask.fresh(self, self.count)
 
     @property
     def count(self) -> int:
@@ -278,6 +328,10 @@ class PackedKeyBatch:
         return k
 
 
+for _cls in (EqKeyBatch, CmpKeyBatch, PackedKeyBatch):
+    _cls.consumed = _ConsumedMask()   # after @dataclass: __init__ keeps its consumed=None default
+
+
 def _eval_packed(party: int, k: PackedKeyBatch, x, out, m_own=None, m_peer=None):
     """Evaluation straight from payload rows (fss_dcf/dpf_eval_packed)."""
     k.validate()
@@ -322,6 +376,11 @@ def _take_unused(batch, m: int):
     consumed[h : h+m] are all free they ARE the first m free keys and go out as
     one contiguous zero-copy slice in O(m); otherwise the full scan is used.
     The handed-out batch is spent: its mask is a read-only all-True view."""
+    if isinstance(getattr(type(batch), "consumed", None), _ConsumedMask):
+        lo = _ConsumedMask.take_prefix(batch, m)
+        if lo is not None:                 # O(1): no mask scan, no mask write now
+            batch._free_hint = lo + m
+            return batch.take(slice(lo, lo + m), _consumed=_spent(m))
     consumed = batch.consumed
     count = consumed.shape[0]
     h = min(getattr(batch, "_free_hint", 0), count)

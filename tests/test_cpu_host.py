@@ -233,3 +233,46 @@ def test_level_stride_and_ring_random_arguments_rejected_without_gpu():
     assert b"null" in lib.fss_last_error()
     st = _lib.PcgState()
     assert lib.fss_pcg64_ring_random(ctypes.byref(st), 32, 8, None, None, None) == 1
+
+
+def test_lazy_consumed_mask_is_exact():
+    """The O(1) take_unused path (pure-prefix masks) records hand-outs and
+    writes them on the next read of ``consumed``; mixed with in-place edits,
+    audits and the scanning path it must always equal an eager mask."""
+    from paper_2006_04593_b200 import fss
+
+    class Rows:                       # stands in for the device arrays
+        def __init__(self, n):
+            self.shape = (n,)
+
+        def __getitem__(self, sel):
+            return Rows(len(range(*sel.indices(self.shape[0]))) if isinstance(sel, slice) else len(sel))
+
+    rng = np.random.default_rng(1)
+    for trial in range(100):
+        n = int(rng.integers(1, 60))
+        b = fss.PackedKeyBatch(1, 0, 8, Rows(n))
+        b.take = lambda idx, _consumed=None, b=b: type("V", (), {"consumed": _consumed, "idx": idx})()
+        ref = np.zeros(n, dtype=bool)
+        for _ in range(10):
+            r = rng.random()
+            if r < 0.15:                                   # in-place edit by a caller
+                pick = rng.integers(0, n, 2)
+                b.consumed[pick] = True
+                ref[pick] = True
+            elif r < 0.25:
+                assert np.array_equal(b.consumed, ref)     # read: flushes
+            else:
+                m = int(rng.integers(0, 6))
+                free = np.flatnonzero(~ref)
+                if free.size < m:
+                    with pytest.raises(fss.KeyExhaustedError):
+                        fss._take_unused(b, m)
+                    continue
+                v = fss._take_unused(b, m)
+                got = v.idx
+                got = np.arange(got.start, got.stop) if isinstance(got, slice) else np.asarray(got)
+                assert np.array_equal(got, free[:m])
+                assert v.consumed.all() and v.consumed.shape == (m,)
+                ref[free[:m]] = True
+        assert np.array_equal(b.consumed, ref)

@@ -46,3 +46,24 @@ def test_two_rank_bench_contract():
     assert g["elements"] == 2 << 18 and g["bytes_to_rank0_wire"] == 2 * (2 << 18) * 4
     assert g["eval_only_ms_per_step"] > 0 and g["nccl_gather_ms_per_step"] > 0
     assert g["peer_fused_ms_per_step"] > 0
+
+
+def test_strong_scaling_mode_self_launched():
+    """`python bench.py --gpus 2 --global-log2n G` without a launcher re-launches
+    itself with 2 ranks (same-GPU gloo mode here) and reports ONE strong-scaling
+    line over the 2^G batch, each rank streaming its slice in chunks."""
+    env = dict(os.environ, FSS_BENCH_SAME_GPU="1")
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k, None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3",
+                        "--warmup", "3", "--global-log2n", "18", "--chunk-log2n", "16"],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["config"]["global_batch"] == 1 << 18
+    c = d["chunking"]
+    assert c["keys_per_rank"] == 1 << 17 and c["chunks_per_rank"] == 2 and not c["resident"]
+    assert d["gpu_launches"] == 3 * 2 * 2 and d["value"] > 0 and d["keygen"]["pairs_per_s"] > 0
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 2 * 8 << 18
