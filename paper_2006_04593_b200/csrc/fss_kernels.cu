@@ -859,7 +859,7 @@ std::mutex g_dev_mu;
 DevInfo g_dev[64];
 
 template <typename K>
-int prep_launch(K kernel, int* grid) {
+int prep_launch(K kernel, int* grid, int smem = fssb::kTableBytes) {
     int dev = 0;
     cudaError_t err = cudaGetDevice(&dev);
     if (err != cudaSuccess) return set_err(kEcuda, "cudaGetDevice: %s", cudaGetErrorString(err));
@@ -878,7 +878,7 @@ int prep_launch(K kernel, int* grid) {
     bool done = false;
     for (const void* k : d.attr_done) done |= (k == key);
     if (!done) {
-        err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fssb::kTableBytes);
+        err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (err != cudaSuccess) return set_err(kEcuda, "cudaFuncSetAttribute: %s", cudaGetErrorString(err));
         d.attr_done.push_back(key);
     }
