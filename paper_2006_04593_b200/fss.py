@@ -199,10 +199,10 @@ class EqKeyBatch:
 
     def take(self, idx, _consumed=None) -> "EqKeyBatch":
         sel, arr = _index(idx, self.count, self.device)
-        return EqKeyBatch(self.party, self.n_bits, _take1(self.alpha_share, sel),
-                          _take1(self.seed0, sel), _take2(self.scw, sel), _take2(self.tcw, sel),
-                          _take1(self.cw_final, sel),
-                          self.consumed[arr].copy() if _consumed is None else _consumed)
+        return _inherit_ready(self, EqKeyBatch(
+            self.party, self.n_bits, _take1(self.alpha_share, sel), _take1(self.seed0, sel),
+            _take2(self.scw, sel), _take2(self.tcw, sel), _take1(self.cw_final, sel),
+            self.consumed[arr].copy() if _consumed is None else _consumed), sel)
 
     def take_unused(self, m: int) -> "EqKeyBatch":
         return _take_unused(self, m)
@@ -249,10 +249,11 @@ class CmpKeyBatch:
 
     def take(self, idx, _consumed=None) -> "CmpKeyBatch":
         sel, arr = _index(idx, self.count, self.device)
-        return CmpKeyBatch(self.party, self.n_bits, _take1(self.alpha_share, sel),
-                           _take1(self.seed0, sel), _take2(self.scw, sel), _take2(self.tcw, sel),
-                           _take2(self.sigma_cw, sel), _take2(self.leaf_cw, sel),
-                           self.consumed[arr].copy() if _consumed is None else _consumed, self.out_bits)
+        return _inherit_ready(self, CmpKeyBatch(
+            self.party, self.n_bits, _take1(self.alpha_share, sel), _take1(self.seed0, sel),
+            _take2(self.scw, sel), _take2(self.tcw, sel), _take2(self.sigma_cw, sel),
+            _take2(self.leaf_cw, sel), self.consumed[arr].copy() if _consumed is None else _consumed,
+            self.out_bits), sel)
 
     def take_unused(self, m: int) -> "CmpKeyBatch":
         return _take_unused(self, m)
@@ -650,6 +651,43 @@ def _eval_operands(k, names):
     return ld
 
 
+_EQ_LEVEL = ("tcw",)
+_CMP_LEVEL = ("tcw", "sigma_cw", "leaf_cw")
+
+
+def _ready_key(k):
+    """Identity of a batch's arrays (objects and shapes): while it is
+    unchanged, validate() and the level-stride probe need not run again."""
+    extra = (k.cw_final,) if isinstance(k, EqKeyBatch) else (k.sigma_cw, k.leaf_cw, k.out_bits)
+    return (k.n_bits, k.alpha_share, k.alpha_share.shape, k.seed0, k.seed0.shape, k.scw, k.scw.shape,
+            k.tcw, k.tcw.shape) + tuple((t, t.shape) if isinstance(t, torch.Tensor) else t for t in extra)
+
+
+def _ready(k, names) -> int:
+    """validate() + the common level stride of the level-major arrays, cached
+    on the batch while its arrays stay the same objects; a contiguous take()
+    of a ready batch inherits it (column views keep the level stride), so the
+    batches take_unused hands to the online protocols skip both."""
+    c = k.__dict__.get("_ready")
+    if c is not None and _same_key(c[0], _ready_key(k)):
+        return c[1]
+    k.validate()
+    ld = _eval_operands(k, names)
+    k.__dict__["_ready"] = (_ready_key(k), ld)
+    return ld
+
+
+def _same_key(a, b) -> bool:
+    return len(a) == len(b) and all(x is y or (type(x) is not torch.Tensor and x == y) for x, y in zip(a, b))
+
+
+def _inherit_ready(parent, child, sel):
+    c = parent.__dict__.get("_ready")
+    if isinstance(sel, slice) and c is not None and _same_key(c[0], _ready_key(parent)):
+        child.__dict__["_ready"] = (_ready_key(child), c[1])
+    return child
+
+
 # Host-tensor inputs at least this large are streamed through the GPU in
 # chunks on two CUDA streams, so the H2D copy of x, the evaluation kernel and
 # the D2H copy of the shares of consecutive chunks overlap.
@@ -743,11 +781,10 @@ def eval_eq(party: int, k: EqKeyBatch, x, out=None):
     ``out``: as for eval_cmp. ``k`` may be a PackedKeyBatch."""
     if isinstance(k, PackedKeyBatch):
         return _eval_packed(party, k, x, out)
-    k.validate()
+    ld = _ready(k, _EQ_LEVEL)
     n, count, dev = k.n_bits, k.count, k.device
     out = _check_out(out, count, dev)
     xt, host = _prep_x(x, count, n, dev)
-    ld = _eval_operands(k, ("tcw",))
     seed0, cw_final = k.seed0.contiguous(), k.cw_final.contiguous()
 
     def launch(lo, hi, xd, od, stream):
@@ -777,13 +814,12 @@ def eval_cmp(party: int, k: CmpKeyBatch, x, return_levels: bool = False, out=Non
         if return_levels:
             return eval_cmp(party, k.unpack(), x, return_levels=True)
         return _eval_packed(party, k, x, out)
-    k.validate()
+    ld = _ready(k, _CMP_LEVEL)
     n, count, dev = k.n_bits, k.count, k.device
     out = _check_out(out, count, dev)
     if out is not None and return_levels:
         raise ValueError("out= and return_levels are exclusive")
     xt, host = _prep_x(x, count, n, dev)
-    ld = _eval_operands(k, ("tcw", "sigma_cw", "leaf_cw"))
     seed0 = k.seed0.contiguous()
     if return_levels:
         if host == "torch_pinned":
@@ -843,9 +879,8 @@ def _masked_round(session, y, alpha_share, n: int, op: str):
 def _eval_cmp_masked(party: int, k: CmpKeyBatch, m_own, m_peer) -> torch.Tensor:
     if isinstance(k, PackedKeyBatch):
         return _eval_packed(party, k, None, None, m_own, m_peer)
-    k.validate()
+    ld = _ready(k, _CMP_LEVEL)
     dev = k.device
-    ld = _eval_operands(k, ("tcw", "sigma_cw", "leaf_cw"))
     seed0 = k.seed0.contiguous()
     out = torch.empty(k.count, dtype=torch.uint64, device=dev)
     with torch.cuda.device(dev):
@@ -859,9 +894,8 @@ def _eval_cmp_masked(party: int, k: CmpKeyBatch, m_own, m_peer) -> torch.Tensor:
 def _eval_eq_masked(party: int, k: EqKeyBatch, m_own, m_peer) -> torch.Tensor:
     if isinstance(k, PackedKeyBatch):
         return _eval_packed(party, k, None, None, m_own, m_peer)
-    k.validate()
+    ld = _ready(k, _EQ_LEVEL)
     dev = k.device
-    ld = _eval_operands(k, ("tcw",))
     seed0, cw_final = k.seed0.contiguous(), k.cw_final.contiguous()
     out = torch.empty(k.count, dtype=torch.uint64, device=dev)
     with torch.cuda.device(dev):

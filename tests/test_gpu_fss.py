@@ -416,3 +416,26 @@ def test_pinned_noncontiguous_input_is_uploaded_not_read_in_place():
     got = fss.eval_cmp(0, k0, xv)
     want = fss.eval_cmp(0, k0, xv.contiguous().cuda())
     assert torch.equal(torch.as_tensor(got).view(torch.int64).cpu().reshape(-1), want.view(torch.int64).cpu())
+
+
+def test_ready_cache_follows_the_arrays():
+    # validate() + level-stride probe are cached per batch while its arrays are
+    # the same objects; take() views inherit it; replacing an array revalidates
+    rng = np.random.default_rng(21)
+    alpha, k0, k1 = fss.keygen_cmp(16, rng, count=64)
+    x = alpha.clone()
+    y = fss.eval_cmp(0, k0, x)
+    assert "_ready" in k0.__dict__
+    sub = k0.take_unused(40)
+    assert "_ready" in sub.__dict__ and sub.__dict__["_ready"][1] == 64      # parent's level stride
+    assert torch.equal(fss.eval_cmp(0, sub, x[:40]).view(torch.int64), y[:40].view(torch.int64))
+    gathered = k0.take(np.array([5, 1, 60]))                                # gather: no inheritance
+    assert "_ready" not in gathered.__dict__
+    assert torch.equal(fss.eval_cmp(0, gathered, x[[5, 1, 60]]).view(torch.int64),
+                       y[[5, 1, 60]].view(torch.int64))
+    k0.scw = k0.scw[:-1]
+    with pytest.raises(fss.KeyFormatError):
+        fss.eval_cmp(0, k0, x)
+    k1.leaf_cw = k1.leaf_cw.clone()                                        # same shape, new object
+    assert torch.equal(fss.eval_cmp(1, k1, x).view(torch.int64),
+                       fss.eval_cmp(1, k1.take(slice(0, 64)), x).view(torch.int64))
