@@ -431,8 +431,9 @@ def test_ready_cache_follows_the_arrays():
     assert torch.equal(fss.eval_cmp(0, sub, x[:40]).view(torch.int64), y[:40].view(torch.int64))
     gathered = k0.take(np.array([5, 1, 60]))                                # gather: no inheritance
     assert "_ready" not in gathered.__dict__
-    assert torch.equal(fss.eval_cmp(0, gathered, x[[5, 1, 60]]).view(torch.int64),
-                       y[[5, 1, 60]].view(torch.int64))
+    pick = torch.tensor([5, 1, 60], device=x.device)
+    assert torch.equal(fss.eval_cmp(0, gathered, x.view(torch.int64)[pick]).view(torch.int64),
+                       y.view(torch.int64)[pick])
     k0.scw = k0.scw[:-1]
     with pytest.raises(fss.KeyFormatError):
         fss.eval_cmp(0, k0, x)
