@@ -497,6 +497,7 @@ class _PartyWorkers:
         self._jobs = [queue.SimpleQueue(), queue.SimpleQueue()]
         self._done = [queue.SimpleQueue(), queue.SimpleQueue()]
         self.lock = threading.Lock()
+        self.pid = os.getpid()
         self.threads = [threading.Thread(target=self._loop, args=(p,), daemon=True,
                                          name=f"ariann-party{p}") for p in (0, 1)]
         for t in self.threads:
@@ -523,7 +524,8 @@ _WORKERS_INIT = threading.Lock()
 def _party_workers():
     global _WORKERS
     with _WORKERS_INIT:
-        if _WORKERS is None:
+        # a forked child inherits the object but not the threads: start anew
+        if _WORKERS is None or _WORKERS.pid != os.getpid():
             _WORKERS = _PartyWorkers()
         return _WORKERS
 

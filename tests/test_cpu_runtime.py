@@ -217,3 +217,25 @@ def test_local_pair_reuses_workers_and_handles_nesting_and_errors():
     for t in ts:
         t.join()
     assert out == [1, 1, 1, 1]
+
+
+def _forked_child(q):
+    def prog(session):
+        return int(session.exchange("x", runtime.FRAME_MASKED,
+                                    torch.full((1,), 7 + session.party, dtype=torch.int32), 1)[0])
+    (a, _), (b, _) = runtime.run_local_pair(prog)
+    q.put((a, b))
+
+
+def test_local_pair_after_fork():
+    # the parent's persistent workers do not exist in a forked child
+    def prog(session):
+        return session.party
+    runtime.run_local_pair(prog)                      # parent starts its workers
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+    p = ctx.Process(target=_forked_child, args=(q,))
+    p.start()
+    assert q.get(timeout=60) == (8, 7)
+    p.join(timeout=30)
+    assert p.exitcode == 0
