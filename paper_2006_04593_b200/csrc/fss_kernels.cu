@@ -319,12 +319,23 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
 // read with 16-byte loads: the lanes of a warp read 32 different records, so
 // each load instruction costs ~32 L1 wavefronts whatever its width -- and the
 // L1 data path is shared with the T-table lookups. Only the aligned 16-byte
-// chunks that hold wanted bytes are loaded (the last record of the last
-// element never reads past the payload); the realignment by the record's
-// offset (uniform across a warp when the record stride is a multiple of 16)
-// is a switch over the 4 word offsets with funnel shifts for the byte offset.
+// chunks that hold wanted bytes are loaded; for the last element of the
+// payload (lim = payload end, else NULL) a chunk that would extend past the end
+// is read byte by byte up to it, so no byte outside the payload is read
+// (compute-sanitizer initcheck: the allocation's slack is never initialised).
+// The realignment by the record's offset (uniform across a warp when the
+// record stride is a multiple of 16) is a switch over the 4 word offsets with
+// funnel shifts for the byte offset.
+__device__ __noinline__ uint4 ld_chunk_tail(const uint4* a, const uint8_t* lim) {
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(a);
+    uint32_t w[4] = {0, 0, 0, 0};
+    for (int i = 0; i < 16 && b + i < lim; i++) w[i >> 2] |= (uint32_t)__ldg(b + i) << (8 * (i & 3));
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 template <int NB>
-__device__ __forceinline__ void ld_stream(const uint8_t* p, uint32_t (&o)[(NB + 3) / 4]) {
+__device__ __forceinline__ void ld_stream(const uint8_t* p, uint32_t (&o)[(NB + 3) / 4],
+                                          const uint8_t* lim = nullptr) {
     constexpr int NO = (NB + 3) / 4, NC = (NB + 30) / 16;   // output words, chunks touched at worst
     const uint4* a = reinterpret_cast<const uint4*>((uintptr_t)p & ~(uintptr_t)15);
     const uint32_t off = (uint32_t)(uintptr_t)p & 15u;
@@ -333,7 +344,10 @@ __device__ __forceinline__ void ld_stream(const uint8_t* p, uint32_t (&o)[(NB + 
     uint32_t w[4 * NC + 4];
 #pragma unroll
     for (int c = 0; c < NC; c++) {
-        const uint4 v = (uint32_t)c <= last ? __ldg(a + c) : make_uint4(0, 0, 0, 0);
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if ((uint32_t)c <= last)
+            v = (lim && reinterpret_cast<const uint8_t*>(a + c + 1) > lim) ? ld_chunk_tail(a + c, lim)
+                                                                           : __ldg(a + c);
         w[4 * c] = v.x;
         w[4 * c + 1] = v.y;
         w[4 * c + 2] = v.z;
@@ -354,9 +368,9 @@ __device__ __forceinline__ void ld_stream(const uint8_t* p, uint32_t (&o)[(NB + 
 
 // A W-byte little-endian ring value at p.
 template <int W>
-__device__ __forceinline__ uint64_t ld_ring(const uint8_t* p) {
+__device__ __forceinline__ uint64_t ld_ring(const uint8_t* p, const uint8_t* lim = nullptr) {
     uint32_t o[(W + 3) / 4];
-    ld_stream<W>(p, o);
+    ld_stream<W>(p, o, lim);
     uint64_t v = o[0];
     if (W > 4) v |= (uint64_t)o[(W + 3) / 4 - 1] << 32;
     return W >= 8 ? v : v & ((1ULL << (8 * W)) - 1);
@@ -378,21 +392,22 @@ dcf_eval_packed_kernel(int party, int n, uint64_t count, const uint8_t* __restri
     const Span sp = cta_span(count);
     for (uint64_t e = sp.lo + threadIdx.x; e < sp.hi; e += blockDim.x) {
         const uint8_t* kp = payload + e * EB;
+        const uint8_t* lim = e + 1 == count ? kp + EB : nullptr;   // payload end
         uint32_t sw[4];
-        ld_stream<16>(kp + W, sw);
+        ld_stream<16>(kp + W, sw, lim);
         U4 s = U4{sw[0], sw[1], sw[2], sw[3]};
         uint32_t t = party;
         uint64_t acc = 0;
         const uint64_t xe = load_x(x, m_own, m_peer, n, e) & mask;
         for (int i = 0; i < n; i++) {
             uint32_t o[NW];
-            ld_stream<rec>(kp + W + 16 + (uint32_t)i * rec, o);
+            ld_stream<rec>(kp + W + 16 + (uint32_t)i * rec, o, lim);
             const U4 cw = U4{o[0], o[1], o[2], o[3]};
             const uint32_t f = o[4] & 0xFFu;
             uint64_t sig = (uint64_t)__funnelshift_r(o[4], NW > 5 ? o[5] : 0u, 8);
             if (W > 3) sig |= (uint64_t)__funnelshift_r(NW > 5 ? o[5] : 0u, NW > 6 ? o[6] : 0u, 8) << 32;
             if (W < 8) sig &= (1ULL << (8 * W)) - 1;
-            const uint64_t leaf = ld_ring<W>(kp + tail + (uint32_t)i * W);
+            const uint64_t leaf = ld_ring<W>(kp + tail + (uint32_t)i * W, lim);
             const uint32_t xb = (uint32_t)(xe >> (n - 1 - i)) & 1u;
             const U4 a = fssb::mmo<0, true>(tb, s, 0u - xb);
             const uint32_t tm = 0u - t;
@@ -407,7 +422,7 @@ dcf_eval_packed_kernel(int party, int n, uint64_t count, const uint8_t* __restri
             s.w &= 0x7FFFFFFFu;
             t = tn;
         }
-        acc += (ld_ring<W>(kp + tail + (uint32_t)n * W) & (0 - (uint64_t)t)) + lo64(s);
+        acc += (ld_ring<W>(kp + tail + (uint32_t)n * W, lim) & (0 - (uint64_t)t)) + lo64(s);
         out[e] = (party ? (0 - acc) : acc) & mask;
     }
 }
@@ -425,14 +440,15 @@ dpf_eval_packed_kernel(int party, int n, uint64_t count, const uint8_t* __restri
     const Span sp = cta_span(count);
     for (uint64_t e = sp.lo + threadIdx.x; e < sp.hi; e += blockDim.x) {
         const uint8_t* kp = payload + e * EB;
+        const uint8_t* lim = e + 1 == count ? kp + EB : nullptr;   // payload end
         uint32_t sw[4];
-        ld_stream<16>(kp + W, sw);
+        ld_stream<16>(kp + W, sw, lim);
         U4 s = U4{sw[0], sw[1], sw[2], sw[3]};
         uint32_t t = party;
         const uint64_t xe = load_x(x, m_own, m_peer, n, e) & mask;
         for (int i = 0; i < n; i++) {
             uint32_t o[5];
-            ld_stream<17>(kp + W + 16 + 17u * i, o);
+            ld_stream<17>(kp + W + 16 + 17u * i, o, lim);
             const U4 cw = U4{o[0], o[1], o[2], o[3]};
             const uint32_t f = o[4] & 0xFFu;
             const uint32_t xb = (uint32_t)(xe >> (n - 1 - i)) & 1u;
@@ -442,7 +458,7 @@ dpf_eval_packed_kernel(int party, int n, uint64_t count, const uint8_t* __restri
             s.w &= 0x7FFFFFFFu;
             t = tn;
         }
-        const uint64_t cwf = ld_ring<W>(kp + W + 16 + 17u * n);
+        const uint64_t cwf = ld_ring<W>(kp + W + 16 + 17u * n, lim);
         uint64_t o = (((uint64_t)t * cwf) + lo64(s)) & mask;
         if (party) o = (0 - o) & mask;
         out[e] = o;
