@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define FSS_ABI_VERSION 4
+#define FSS_ABI_VERSION 5
 #define FSS_OK 0
 #define FSS_EINVAL 1
 #define FSS_ECUDA 2
@@ -225,6 +225,34 @@ int fss_memcpy_d2d(void* dst, const void* src, uint64_t nbytes, void* stream);
 int fss_ipc_get_handle(const void* dev_ptr, uint8_t* handle);
 int fss_ipc_open_handle(const uint8_t* handle, void** dev_ptr);
 int fss_ipc_close_handle(void* dev_ptr);
+
+/* Host scheduling words of the in-process two-party runtime
+ * (runtime.run_local_pair; the reference runs its two parties as two threads
+ * over blocking queues, runtime.py:285-311). Not a reference entry point.
+ * fss_host_wait first adds 1 to *bump (if not NULL) and stores pass_to into
+ * *turn (if turn != NULL and pass_to >= 0), then waits -- callers drop the GIL
+ * for the call -- until *word >= target and, for at most grace_s after that,
+ * until *turn == me (turn NULL or me < 0: no turn condition). It spins for
+ * spin_s, then yields for spin_s, then naps (<= 50 us); once *word >= target
+ * it spins. Returns 0, 1 after timeout_s, FSS_EINVAL for a NULL word.
+ * load / store / add are acquire / release / acq_rel atomics on one word. */
+int64_t fss_host_load(const int64_t* word);
+void fss_host_store(int64_t* word, int64_t value);
+int64_t fss_host_add(int64_t* word, int64_t delta);
+int fss_host_wait(const int64_t* word, int64_t target, int64_t* turn, int64_t me, int64_t pass_to,
+                  int64_t* bump, double spin_s, double grace_s, double timeout_s);
+
+/* Stream ordering for the in-process pair (not a reference entry point):
+ * timing-free events, and fss_streams_link -- the first n_waiters of
+ * (waiter0, waiter1) wait for the work queued so far on the first n_producers
+ * of (producer0, producer1) (streams of the current device, 0 = the legacy
+ * default stream); run_local_pair forks / joins the party streams with it. */
+int fss_event_create(void** ev);
+int fss_event_destroy(void* ev);
+int fss_event_record(void* ev, void* stream);
+int fss_stream_wait_event(void* stream, void* ev);
+int fss_streams_link(void* waiter0, void* waiter1, int n_waiters, void* producer0, void* producer1,
+                     int n_producers);
 
 /* Diagnostics (not a reference entry point): on-box peak probes used as the
  * roofline denominators of the AES work. Synchronous; runs ~10 ms of probe

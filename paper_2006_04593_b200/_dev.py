@@ -3,6 +3,8 @@ pointers and the current CUDA stream handed to the C ABI."""
 
 from __future__ import annotations
 
+import contextlib
+
 import numpy as np
 import torch
 
@@ -42,8 +44,29 @@ def side_streams(device: torch.device, k: int = 2) -> list:
     return got[:k]
 
 
+try:
+    _raw_stream = torch._C._cuda_getCurrentRawStream   # the cudaStream_t, without a Stream object
+except AttributeError:  # pragma: no cover - older torch
+    _raw_stream = None
+
+
 def stream_handle(device: torch.device) -> int:
+    """cudaStream_t of the calling thread's current stream on ``device``."""
+    if _raw_stream is not None and device.index is not None:
+        return _raw_stream(device.index)
     return torch.cuda.current_stream(device).cuda_stream
+
+
+_NULL_CTX = contextlib.nullcontext()
+
+
+def on(device):
+    """``torch.cuda.device(device)``, skipped (a shared no-op context) when
+    that device is already the calling thread's current one."""
+    idx = device if isinstance(device, int) else getattr(device, "index", None)
+    if idx is not None and torch._C._cuda_getDevice() == idx:
+        return _NULL_CTX
+    return torch.cuda.device(device)
 
 
 def ptr(t) -> int | None:

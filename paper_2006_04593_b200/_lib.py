@@ -33,7 +33,7 @@ class Peaks(ctypes.Structure):
 
 
 # name -> argtypes (all return int status unless listed in _RESTYPE)
-ABI_VERSION = 4   # include/ariann_fss.h FSS_ABI_VERSION
+ABI_VERSION = 5   # include/ariann_fss.h FSS_ABI_VERSION
 
 SIGNATURES = {
     "fss_abi_version": [],
@@ -72,8 +72,19 @@ SIGNATURES = {
     "fss_ipc_get_handle": [_vp, _vp],
     "fss_ipc_open_handle": [_vp, ctypes.POINTER(ctypes.c_void_p)],
     "fss_ipc_close_handle": [_vp],
+    "fss_event_create": [ctypes.POINTER(ctypes.c_void_p)],
+    "fss_event_destroy": [_vp],
+    "fss_event_record": [_vp, _vp],
+    "fss_stream_wait_event": [_vp, _vp],
+    "fss_streams_link": [_vp, _vp, _int, _vp, _vp, _int],
+    "fss_host_load": [_vp],
+    "fss_host_store": [_vp, ctypes.c_int64],
+    "fss_host_add": [_vp, ctypes.c_int64],
+    "fss_host_wait": [_vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int64, _vp, ctypes.c_double,
+                      ctypes.c_double, ctypes.c_double],
 }
-_RESTYPE = {"fss_last_error": ctypes.c_char_p, "fss_arnk_elem_bytes": ctypes.c_uint64}
+_RESTYPE = {"fss_last_error": ctypes.c_char_p, "fss_arnk_elem_bytes": ctypes.c_uint64,
+            "fss_host_load": ctypes.c_int64, "fss_host_store": None, "fss_host_add": ctypes.c_int64}
 
 _lib = None
 

@@ -183,7 +183,7 @@ def beaver_protocol(session: Session, x: AdditiveShare, y: AdditiveShare,
         raise ValueError("peer payload size mismatch")
     peer = peer.to(dev).reshape(-1)
     z = torch.empty(m, dtype=torch.uint64, device=dev)
-    with torch.cuda.device(dev):
+    with _dev.on(dev):
         _lib.call("fss_beaver_mul", t.party, n, m, _dev.ptr(wire[:m]), _dev.ptr(peer[:m]),
                   _dev.ptr(wire[m:]), _dev.ptr(peer[m:]), _dev.ptr(ta), _dev.ptr(tb),
                   _dev.ptr(tc), _dev.ptr(z), _dev.stream_handle(dev))

@@ -340,7 +340,7 @@ def _eval_packed(party: int, k: PackedKeyBatch, x, out, m_own=None, m_peer=None)
     n, count, dev = k.n_bits, k.count, k.device
     if m_own is not None:          # the masked round's opening happens in the kernel
         res = torch.empty(count, dtype=torch.uint64, device=dev)
-        with torch.cuda.device(dev):
+        with _dev.on(dev):
             _lib.call(fn, int(party), n, count, _dev.ptr(k.payload), None, _dev.ptr(m_own),
                       _dev.ptr(m_peer), _dev.ptr(res), _dev.stream_handle(dev))
         return res
@@ -348,7 +348,7 @@ def _eval_packed(party: int, k: PackedKeyBatch, x, out, m_own=None, m_peer=None)
     xt, host = _prep_x(x, count, n, dev)
 
     def launch(lo, hi, xd, od, stream):
-        with torch.cuda.device(dev):
+        with _dev.on(dev):
             _lib.call(fn, int(party), n, hi - lo, _dev.ptr(k.payload[lo:hi]), _dev.ptr(xd), None, None,
                       _dev.ptr(od), stream)
     return _run_eval(launch, xt, host, count, dev, None, out)
@@ -438,7 +438,7 @@ def _sample_tape(n: int, rng, count: int, alpha, device, shard=None):
         s1 = torch.empty((count, 16), dtype=torch.uint8, device=device)
         cst, st = _pcg.snapshot(rng)
         out_st = PcgState()
-        with torch.cuda.device(device):
+        with _dev.on(device):
             _lib.call("fss_pcg64_seeds", cst, count, _dev.ptr(s0), _dev.ptr(s1), out_st,
                       _dev.stream_handle(device))
         _pcg.commit(rng, st, out_st, count > 0)
@@ -454,7 +454,7 @@ def _sample_tape(n: int, rng, count: int, alpha, device, shard=None):
     a0 = torch.empty(count, dtype=torch.uint64, device=device)
     s0 = torch.empty((count, 16), dtype=torch.uint8, device=device)
     s1 = torch.empty((count, 16), dtype=torch.uint8, device=device)
-    with torch.cuda.device(device):
+    with _dev.on(device):
         _lib.call("fss_pcg64_tape", cst, n, count, int(draw_alpha),
                   _dev.ptr(a) if draw_alpha else None, _dev.ptr(a0), _dev.ptr(s0), _dev.ptr(s1),
                   out_st, _dev.stream_handle(device))
@@ -487,7 +487,7 @@ def _sample_tape_slice(n: int, rng, count: int, alpha, device, lo: int, m: int):
     a0 = torch.empty(m, dtype=torch.uint64, device=device)
     s0 = torch.empty((m, 16), dtype=torch.uint8, device=device)
     s1 = torch.empty((m, 16), dtype=torch.uint8, device=device)
-    with torch.cuda.device(device):
+    with _dev.on(device):
         _lib.call("fss_pcg64_tape_slice", cst, n, count, lo, m, int(draw_alpha),
                   _dev.ptr(a) if draw_alpha else None, _dev.ptr(a0), _dev.ptr(s0), _dev.ptr(s1),
                   out_st, _dev.stream_handle(device))
@@ -525,7 +525,7 @@ def _keygen_eq_core(n: int, alpha, alpha0, s0_init, s1_init):
     tcw = torch.empty((n, count), dtype=torch.uint8, device=dev)
     cw_final = torch.empty(count, dtype=torch.uint64, device=dev)
     alpha1 = torch.empty(count, dtype=torch.uint64, device=dev)
-    with torch.cuda.device(dev):
+    with _dev.on(dev):
         _lib.call("fss_dpf_keygen", n, count, _dev.ptr(alpha), _dev.ptr(alpha0), _dev.ptr(s0_init),
                   _dev.ptr(s1_init), _dev.ptr(scw), _dev.ptr(tcw), _dev.ptr(cw_final),
                   _dev.ptr(alpha1), _dev.stream_handle(dev))
@@ -546,7 +546,7 @@ def _keygen_cmp_core(n: int, alpha, alpha0, s0_init, s1_init, out_bits: int = No
     sigma_cw = torch.empty((n, count), dtype=torch.uint64, device=dev)
     leaf_cw = torch.empty((n + 1, count), dtype=torch.uint64, device=dev)
     alpha1 = torch.empty(count, dtype=torch.uint64, device=dev)
-    with torch.cuda.device(dev):
+    with _dev.on(dev):
         _lib.call("fss_dcf_keygen", n, out_bits, count, _dev.ptr(alpha), _dev.ptr(alpha0),
                   _dev.ptr(s0_init), _dev.ptr(s1_init), _dev.ptr(scw), _dev.ptr(tcw),
                   _dev.ptr(sigma_cw), _dev.ptr(leaf_cw), _dev.ptr(alpha1), _dev.stream_handle(dev))
@@ -656,11 +656,13 @@ _CMP_LEVEL = ("tcw", "sigma_cw", "leaf_cw")
 
 
 def _ready_key(k):
-    """Identity of a batch's arrays (objects and shapes): while it is
-    unchanged, validate() and the level-stride probe need not run again."""
-    extra = (k.cw_final,) if isinstance(k, EqKeyBatch) else (k.sigma_cw, k.leaf_cw, k.out_bits)
-    return (k.n_bits, k.alpha_share, k.alpha_share.shape, k.seed0, k.seed0.shape, k.scw, k.scw.shape,
-            k.tcw, k.tcw.shape) + tuple((t, t.shape) if isinstance(t, torch.Tensor) else t for t in extra)
+    """Identity of a batch's arrays: while the fields hold the same tensor
+    objects, validate() and the level-stride probe need not run again
+    (assigning a field -- the way a batch's arrays are replaced -- changes it;
+    key tensors are never resized in place)."""
+    if isinstance(k, EqKeyBatch):
+        return (k.n_bits, k.alpha_share, k.seed0, k.scw, k.tcw, k.cw_final)
+    return (k.n_bits, k.out_bits, k.alpha_share, k.seed0, k.scw, k.tcw, k.sigma_cw, k.leaf_cw)
 
 
 def _ready(k, names) -> int:
@@ -788,13 +790,13 @@ def eval_eq(party: int, k: EqKeyBatch, x, out=None):
     seed0, cw_final = k.seed0.contiguous(), k.cw_final.contiguous()
 
     def launch(lo, hi, xd, od, stream):
-        with torch.cuda.device(dev):
+        with _dev.on(dev):
             _lib.call("fss_dpf_eval", int(party), n, hi - lo, ld, _dev.ptr(seed0[lo:hi]),
                       _dev.ptr(k.scw[:, lo:hi]), _dev.ptr(k.tcw[:, lo:hi]),
                       _dev.ptr(cw_final[lo:hi]), _dev.ptr(xd), _dev.ptr(od), stream)
 
     def host_launch(xh, oh, xs, os_, chunk, stage, sa, sb):
-        with torch.cuda.device(dev):
+        with _dev.on(dev):
             _lib.call("fss_dpf_eval_host", int(party), n, count, ld, _dev.ptr(seed0),
                       _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(cw_final), xh, oh,
                       _dev.ptr(xs), _dev.ptr(os_), chunk, stage, sa, sb)
@@ -828,21 +830,21 @@ def eval_cmp(party: int, k: CmpKeyBatch, x, return_levels: bool = False, out=Non
             xt, host = torch.from_numpy(xt).to(dev), True
         out = torch.empty(count, dtype=torch.uint64, device=dev)
         levels = torch.empty((n + 1, count), dtype=torch.uint64, device=dev)
-        with torch.cuda.device(dev):
+        with _dev.on(dev):
             _lib.call("fss_dcf_eval", int(party), n, int(k.out_bits), count, ld, _dev.ptr(seed0),
                       _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(k.sigma_cw), _dev.ptr(k.leaf_cw),
                       _dev.ptr(xt), _dev.ptr(out), _dev.ptr(levels), _dev.stream_handle(dev))
         return _result(out, host), _result(levels, host)
 
     def launch(lo, hi, xd, od, stream):
-        with torch.cuda.device(dev):
+        with _dev.on(dev):
             _lib.call("fss_dcf_eval", int(party), n, int(k.out_bits), hi - lo, ld,
                       _dev.ptr(seed0[lo:hi]), _dev.ptr(k.scw[:, lo:hi]), _dev.ptr(k.tcw[:, lo:hi]),
                       _dev.ptr(k.sigma_cw[:, lo:hi]), _dev.ptr(k.leaf_cw[:, lo:hi]), _dev.ptr(xd),
                       _dev.ptr(od), None, stream)
 
     def host_launch(xh, oh, xs, os_, chunk, stage, sa, sb):
-        with torch.cuda.device(dev):
+        with _dev.on(dev):
             _lib.call("fss_dcf_eval_host", int(party), n, int(k.out_bits), count, ld,
                       _dev.ptr(seed0), _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(k.sigma_cw),
                       _dev.ptr(k.leaf_cw), xh, oh, _dev.ptr(xs), _dev.ptr(os_), chunk, stage,
@@ -883,7 +885,7 @@ def _eval_cmp_masked(party: int, k: CmpKeyBatch, m_own, m_peer) -> torch.Tensor:
     dev = k.device
     seed0 = k.seed0.contiguous()
     out = torch.empty(k.count, dtype=torch.uint64, device=dev)
-    with torch.cuda.device(dev):
+    with _dev.on(dev):
         _lib.call("fss_dcf_eval_masked", int(party), k.n_bits, int(k.out_bits), k.count, ld,
                   _dev.ptr(seed0), _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(k.sigma_cw),
                   _dev.ptr(k.leaf_cw), _dev.ptr(m_own), _dev.ptr(m_peer), _dev.ptr(out),
@@ -898,7 +900,7 @@ def _eval_eq_masked(party: int, k: EqKeyBatch, m_own, m_peer) -> torch.Tensor:
     dev = k.device
     seed0, cw_final = k.seed0.contiguous(), k.cw_final.contiguous()
     out = torch.empty(k.count, dtype=torch.uint64, device=dev)
-    with torch.cuda.device(dev):
+    with _dev.on(dev):
         _lib.call("fss_dpf_eval_masked", int(party), k.n_bits, k.count, ld, _dev.ptr(seed0),
                   _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(cw_final), _dev.ptr(m_own),
                   _dev.ptr(m_peer), _dev.ptr(out), _dev.stream_handle(dev))
@@ -998,7 +1000,7 @@ def _pack_device(k) -> torch.Tensor:
     ld = _eval_operands(k, names)
     alpha, seed0 = k.alpha_share.contiguous(), k.seed0.contiguous()
     buf = torch.empty((k.count, elem), dtype=torch.uint8, device=dev)
-    with torch.cuda.device(dev):
+    with _dev.on(dev):
         _lib.call("fss_arnk_pack", kind, k.n_bits, k.count, ld, _dev.ptr(alpha), _dev.ptr(seed0),
                   _dev.ptr(k.scw), _dev.ptr(k.tcw),
                   _dev.ptr(k.cw_final.contiguous()) if kind == KIND_EQ else None,
@@ -1038,7 +1040,7 @@ def _unpack(kind: int, party: int, n: int, count: int, payload, device=None):
     else:
         sigma = torch.empty((n, count), dtype=torch.uint64, device=dev)
         leaf = torch.empty((n + 1, count), dtype=torch.uint64, device=dev)
-    with torch.cuda.device(dev):
+    with _dev.on(dev):
         _lib.call("fss_arnk_unpack", kind, n, count, count, _dev.ptr(buf), _dev.ptr(alpha),
                   _dev.ptr(seed0), _dev.ptr(scw), _dev.ptr(tcw), _dev.ptr(cw_final),
                   _dev.ptr(sigma), _dev.ptr(leaf), _dev.stream_handle(dev))

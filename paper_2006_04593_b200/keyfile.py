@@ -228,7 +228,7 @@ def load_keys(path, party: int = None, device=None, chunk: int = CHUNK, packed: 
                     continue
                 dst = staged[b][: (hi - lo) * elem]
                 dst.copy_(pinned[b][: (hi - lo) * elem], non_blocking=True)
-                with torch.cuda.device(dev):
+                with _dev.on(dev):
                     _lib.call("fss_arnk_unpack", kind, n, hi - lo, count, _dev.ptr(dst),
                               _col(k.alpha_share, lo), _col(k.seed0, lo, 16), _col(k.scw, lo, 16),
                               _col(k.tcw, lo), _col(getattr(k, "cw_final", None), lo),

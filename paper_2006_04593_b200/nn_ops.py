@@ -56,21 +56,28 @@ class MaxpoolK2Prep:
     level2: ReluPrep
 
 
+def _plus_public(x: AdditiveShare, c) -> AdditiveShare:
+    """x.add_public(c) for an operand the protocol consumes right away: party 1
+    passes its share through instead of copying it (values identical; nothing
+    here writes a share in place)."""
+    return x.add_public(c) if x.party == 0 else x
+
+
 def relu(session, x: AdditiveShare, prep: ReluPrep) -> AdditiveShare:
     """max(x, 0) elementwise; exactly 0 at x == 0. Two rounds (nn_ops.py:83-94).
 
     Sign test on x + 1, b = 1 - 1[x <= -1] = 1[x >= 0], then one product b * x."""
-    shifted = AdditiveShare(x.party, x.values, 0).add_public(1)
+    shifted = _plus_public(AdditiveShare(x.party, x.values, 0), 1)
     s = fss.sign_protocol(session, shifted, prep.cmp)
-    b = (-s).add_public(1)
+    b = _plus_public(-s, 1)
     return mul_protocol(session, b, AdditiveShare(x.party, x.values, x.precision), prep.triple)
 
 
 def relu_mask(session, x: AdditiveShare, cmp_keys: fss.CmpKeyBatch) -> AdditiveShare:
     """Shares of 1[x >= 0] only, one round (nn_ops.py:97-101)."""
-    shifted = AdditiveShare(x.party, x.values, 0).add_public(1)
+    shifted = _plus_public(AdditiveShare(x.party, x.values, 0), 1)
     s = fss.sign_protocol(session, shifted, cmp_keys)
-    return (-s).add_public(1)
+    return _plus_public(-s, 1)
 
 
 _OFF_DIAG = {}
@@ -102,7 +109,7 @@ def argmax(session, x: AdditiveShare, prep: ArgmaxPrep) -> AdditiveShare:
     y = AdditiveShare(x.party, RingTensor(_pairwise_diffs(x.values.data, m), x.n_bits), 0)
     s = fss.sign_protocol(session, y, prep.cmp)  # 1[x_i <= x_j]
     counts = s.reshape(*s.shape[:-1], m, m - 1).sum(axis=-1)
-    centered = counts.add_public(-(m - 1))
+    centered = _plus_public(counts, -(m - 1))
     return fss.eq_protocol(session, centered, prep.eq)
 
 
@@ -126,9 +133,11 @@ def maxpool(session, x: AdditiveShare, k: int, prep: MaxpoolPrep, stride: int = 
     kk = k * k
     flat = win.reshape(-1, kk)
     wshare = AdditiveShare(x.party, RingTensor(flat, x.n_bits, _trusted=True), x.precision)
-    bias = torch.arange(kk, device=flat.device, dtype=torch.int64).expand(flat.shape[0], kk)
-    perturbed = wshare.mul_public_int(kk).add_public(
-        RingTensor(_dev.as_u64(bias.contiguous()), x.n_bits, _trusted=True))
+    perturbed = wshare.mul_public_int(kk)
+    if x.party == 0:   # the public in-window index bias (party 1 adds nothing)
+        bias = torch.arange(kk, device=flat.device, dtype=torch.int64).expand(flat.shape[0], kk)
+        perturbed = perturbed.add_public(RingTensor(_dev.as_u64(bias.contiguous()), x.n_bits,
+                                                    _trusted=True))
     onehot = argmax(session, perturbed, prep.argmax)
     prods = mul_protocol(session, onehot, wshare, prep.dot_triple)
     pooled = prods.sum(axis=-1)

@@ -61,7 +61,7 @@ def expand(seeds, out_blocks: int):
     t, dev, host = _seeds_in(seeds)
     n = t.shape[0]
     out = torch.empty((n, out_blocks * BLOCK_BYTES), dtype=torch.uint8, device=dev)
-    with torch.cuda.device(dev):
+    with _dev.on(dev):
         _lib.call("fss_aes_mmo_expand", _dev.ptr(t), n, out_blocks, _dev.ptr(out),
                   _dev.stream_handle(dev))
     return _dev.to_numpy(out) if host else out
@@ -160,7 +160,7 @@ def mask_stream(seed: bytes, round_idx: int, count: int, n_bits: int, device=Non
     lo = int.from_bytes(bytes(seed[:8]), "little")
     hi = int.from_bytes(bytes(seed[8:]), "little")
     out = torch.empty(int(count), dtype=torch.uint64, device=dev)
-    with torch.cuda.device(dev):
+    with _dev.on(dev):
         _lib.call("fss_mask_stream", lo, hi, int(round_idx) & _dev.FULL64, int(count), n_bits,
                   _dev.ptr(out), _dev.stream_handle(dev))
     return out if device is not None else _dev.to_numpy(out)

@@ -24,7 +24,7 @@ def _run(op, a: torch.Tensor, b, n_bits: int) -> torch.Tensor:
         bp, bs = None, (int(b) if b is not None else 0) & _dev.FULL64
     out = torch.empty_like(a)
     dev = a.device
-    with torch.cuda.device(dev):
+    with _dev.on(dev):
         _lib.call("fss_ring_op", _OPS[op], n_bits, a.numel(), _dev.ptr(a), bp, bs, _dev.ptr(out),
                   _dev.stream_handle(dev))
     return out

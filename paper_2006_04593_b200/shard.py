@@ -35,7 +35,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from . import fss
+from . import _dev, fss
 
 
 def shard_bounds(total: int, rank: int, world: int) -> tuple[int, int]:
@@ -171,7 +171,7 @@ class PeerGather:
         hb = _lib.load().fss_ipc_handle_bytes()
         handle = torch.zeros(hb, dtype=torch.uint8)
         self._owned = None
-        with torch.cuda.device(self.device):
+        with _dev.on(self.device):
             if self.rank == self.dst:
                 ptr = ctypes.c_void_p()
                 _lib.call("fss_ipc_alloc", max(8 * self.slots * self.total, 16), ctypes.byref(ptr))
@@ -216,7 +216,7 @@ class PeerGather:
         self._closed = True
         torch.cuda.current_stream(self.device).synchronize()
         self._barrier()                      # nobody writes or reads any more
-        with torch.cuda.device(self.device):
+        with _dev.on(self.device):
             if self.rank == self.dst:
                 self._lib.call("fss_ipc_free", ctypes.c_void_p(self._owned))
             else:

@@ -21,16 +21,28 @@ what = sys.argv[1] if len(sys.argv) > 1 else "relu"
 LOG = []
 
 
+GPU = []   # (thread, label, event before the call, event after it) on the calling stream
+GPU_LABELS = ("_eval_cmp_masked", "_eval_eq_masked", "beaver_protocol")
+
+
 def wrap(mod, name, label=None):
     fn = getattr(mod, name)
 
     @functools.wraps(fn)
     def w(*a, **k):
         t0 = time.perf_counter()
+        gpu = name in GPU_LABELS
+        if gpu:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record()
         try:
             return fn(*a, **k)
         finally:
             LOG.append((threading.current_thread().name, label or name, t0, time.perf_counter()))
+            if gpu:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record()
+                GPU.append((threading.current_thread().name, label or name, e0, e1))
     setattr(mod, name, w)
 
 
@@ -82,22 +94,48 @@ def once():
             return fss.sign_protocol(s, AdditiveShare(s.party, xs[s.party].values, 0), preps[s.party])
         return nn_ops.maxpool(s, xs[s.party], 2, preps[s.party], 2)
     LOG.clear()
+    GPU.clear()
+    start = torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
+    start.record()
     runtime.run_local_pair(prog)
     t1 = time.perf_counter()
+    end = torch.cuda.Event(enable_timing=True)
+    end.record()
     torch.cuda.synchronize()
     t2 = time.perf_counter()
-    return t0, t1, t2
+    gpu = [(th, name, start.elapsed_time(a), start.elapsed_time(b)) for th, name, a, b in GPU]
+    return t0, t1, t2, gpu, start.elapsed_time(end)
 
 
 for _ in range(5):
     once()
-walls = []
-for _ in range(10):
-    t0, t1, t2 = once()
+walls, spans, gspans, gends = [], {}, {}, []
+for _ in range(11):
+    t0, t1, t2, gpu, gend = once()
     walls.append(t2 - t0)
-print(what, "online wall ms: median %.3f" % (sorted(walls)[5] * 1e3))
-print("last run: run_local_pair returned at %.3f ms, GPU done at %.3f ms" % ((t1 - t0) * 1e3, (t2 - t0) * 1e3))
-for th, name, a, b in sorted(LOG, key=lambda r: r[2]):
-    print("  %-12s %-28s %8.3f -> %8.3f  (%.3f ms)" % (th[-12:], name, (a - t0) * 1e3, (b - t0) * 1e3,
-                                                     (b - a) * 1e3))
+    gends.append(gend)
+    seen = {}
+    for th, name, a, b in sorted(LOG, key=lambda r: r[2]):
+        key = (th[-12:], name, seen.setdefault((th, name), 0))
+        seen[(th, name)] += 1
+        spans.setdefault(key, []).append(((a - t0) * 1e3, (b - t0) * 1e3))
+    seen = {}
+    for th, name, a, b in gpu:
+        key = (th[-12:], name, seen.setdefault((th, name), 0))
+        seen[(th, name)] += 1
+        gspans.setdefault(key, []).append((a, b))
+
+
+def med(v):
+    return sorted(v)[len(v) // 2]
+
+
+print(what, "online wall ms: median %.3f over %d runs; GPU start->end event median %.3f ms"
+      % (med(walls) * 1e3, len(walls), med(gends)))
+print("host spans (median start -> median end, ms from the run start):")
+for key, v in sorted(spans.items(), key=lambda kv: med([a for a, _ in kv[1]])):
+    print("  %-12s %-28s %8.3f -> %8.3f" % (key[0], key[1], med([a for a, _ in v]), med([b for _, b in v])))
+print("GPU spans of the same calls (CUDA events on the party stream before / after the call):")
+for key, v in sorted(gspans.items(), key=lambda kv: med([a for a, _ in kv[1]])):
+    print("  %-12s %-28s %8.3f -> %8.3f" % (key[0], key[1], med([a for a, _ in v]), med([b for _, b in v])))

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for sym in declared:
         assert hasattr(lib, sym), sym
     assert set(_lib.SIGNATURES) >= declared
-    assert lib.fss_abi_version() == 4
+    assert lib.fss_abi_version() == 5
     assert not hasattr(lib, "fss_aes_mmo_expand_bitsliced")   # research record, not product ABI
     assert lib.fss_arnk_elem_bytes(1, 32) == 824 and lib.fss_arnk_elem_bytes(0, 32) == 568
     assert isinstance(ctypes.CDLL(_build.LIB), ctypes.CDLL)
@@ -184,7 +184,7 @@ def test_ctypes_signatures_match_header_prototypes():
     with open(os.path.join(ROOT, "include", "ariann_fss.h")) as fh:
         text = re.sub(r"/\*.*?\*/", "", fh.read(), flags=re.S)
     protos = {}
-    for m in re.finditer(r"\b(?:int|uint64_t|const char\*)\s+(fss_\w+)\s*\(([^)]*)\)\s*;", text):
+    for m in re.finditer(r"\b(?:int|int64_t|void|uint64_t|const char\*)\s+(fss_\w+)\s*\(([^)]*)\)\s*;", text):
         params = m.group(2).strip()
         protos[m.group(1)] = 0 if params in ("", "void") else params.count(",") + 1
     assert protos, "no prototypes parsed"
