@@ -212,6 +212,16 @@ int fss_beaver_mul(int party, int n_bits, uint64_t count, const void* delta_own,
                    const uint64_t* a, const uint64_t* b, const uint64_t* c, uint64_t* z,
                    void* stream);
 
+/* argmax's pairwise differences (nn_ops.py:111-114): v is (rows, m) u64;
+ * out is (rows, m*(m-1)) with out[r][j*(m-1)+k] = v[r][i] - v[r][j] mod 2^n,
+ * i running over the indices != j in ascending order. */
+int fss_ring_pairwise(int n_bits, uint64_t rows, int m, const uint64_t* v, uint64_t* out, void* stream);
+
+/* out[q] = (in[q*g] + ... + in[q*g+g-1] + add) mod 2^n for q < groups: argmax's
+ * per-row counts (nn_ops.py:115-116) and maxpool's window sums (:174). */
+int fss_ring_group_sum(int n_bits, uint64_t groups, int g, const uint64_t* in, uint64_t add, uint64_t* out,
+                       void* stream);
+
 /* CUDA IPC for the peer-memory exchange (runtime.PeerTransport): export a
  * device allocation as an opaque handle (fss_ipc_handle_bytes() bytes), map a
  * peer process's allocation (peer access enabled lazily), unmap it. Replaces

@@ -61,6 +61,8 @@ SIGNATURES = {
     "fss_arnk_unpack": [_int, _int, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "fss_ring_op": [_int, _int, _u64, _vp, _vp, _u64, _vp, _vp],
     "fss_beaver_mul": [_int, _int, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "fss_ring_pairwise": [_int, _u64, _int, _vp, _vp, _vp],
+    "fss_ring_group_sum": [_int, _u64, _int, _vp, _u64, _vp, _vp],
     "fss_wire_bytes": [_int],
     "fss_wire_pack": [_int, _int, _u64, _vp, _vp, _vp, _vp],
     "fss_wire_open": [_int, _u64, _vp, _vp, _vp, _vp],

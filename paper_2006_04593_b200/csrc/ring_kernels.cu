@@ -83,6 +83,39 @@ __global__ void beaver_kernel(int party, int wb, uint64_t mask, uint64_t count,
     }
 }
 
+// argmax's pairwise differences (reference nn_ops.py:111-114): for each row of
+// m values, out[j][k] = v[i] - v[j] over the m-1 indices i != j in ascending
+// order (k = i for i < j, i - 1 for i > j), mod 2^n. One thread per output;
+// the row's m values are re-read from L1/L2.
+__global__ void pairwise_kernel(uint64_t mask, uint64_t rows, uint32_t m, const uint64_t* __restrict__ v,
+                                uint64_t* __restrict__ out) {
+    const uint32_t per = m * (m - 1);
+    const uint64_t total = rows * per;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; o < total; o += stride) {
+        const uint64_t r = o / per;
+        const uint32_t w = (uint32_t)(o - r * per);
+        const uint32_t j = w / (m - 1), k = w - j * (m - 1);
+        const uint32_t i = k + (k >= j);
+        const uint64_t* row = v + r * m;
+        out[o] = (__ldg(row + i) - __ldg(row + j)) & mask;
+    }
+}
+
+// out[q] = (sum of the g values in[q*g .. q*g+g) + add) mod 2^n: the per-row
+// counts of argmax (nn_ops.py:115-116, with the public -(m-1) of party 0)
+// and maxpool's window sums (nn_ops.py:174).
+__global__ void group_sum_kernel(uint64_t mask, uint64_t groups, uint32_t g, const uint64_t* __restrict__ in,
+                                 uint64_t add, uint64_t* __restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < groups; q += stride) {
+        const uint64_t* p = in + q * g;
+        uint64_t acc = add;
+        for (uint32_t t = 0; t < g; t++) acc += __ldg(p + t);
+        out[q] = acc & mask;
+    }
+}
+
 int grid_size(uint64_t count) {
     static int sms_of[64] = {0};  // per device; benign race (same value written)
     int dev = 0;
@@ -159,6 +192,29 @@ int fss_beaver_mul(int party, int n_bits, uint64_t count, const void* delta_own,
     beaver_kernel<<<grid_size(count), 256, 0, (cudaStream_t)stream>>>(
         party, fss_wire_bytes(n_bits), mask, count, delta_own, delta_peer, eps_own, eps_peer, a, b,
         c, z);
+    return done();
+}
+
+int fss_ring_pairwise(int n_bits, uint64_t rows, int m, const uint64_t* v, uint64_t* out, void* stream) {
+    if (n_bits < 1 || n_bits > 64) return fssb::set_error(FSS_EINVAL, "ring width out of range");
+    if (m < 2 || m > 65536) return fssb::set_error(FSS_EINVAL, "pairwise: m must be in [2, 65536]");
+    if (rows == 0) return FSS_OK;
+    if (!v || !out) return fssb::set_error(FSS_EINVAL, "null device pointer");
+    const uint64_t mask = n_bits >= 64 ? ~0ULL : ((1ULL << n_bits) - 1);
+    pairwise_kernel<<<grid_size(rows * (uint64_t)m * (m - 1)), 256, 0, (cudaStream_t)stream>>>(
+        mask, rows, (uint32_t)m, v, out);
+    return done();
+}
+
+int fss_ring_group_sum(int n_bits, uint64_t groups, int g, const uint64_t* in, uint64_t add, uint64_t* out,
+                       void* stream) {
+    if (n_bits < 1 || n_bits > 64) return fssb::set_error(FSS_EINVAL, "ring width out of range");
+    if (g < 1) return fssb::set_error(FSS_EINVAL, "group sum: group size must be >= 1");
+    if (groups == 0) return FSS_OK;
+    if (!in || !out) return fssb::set_error(FSS_EINVAL, "null device pointer");
+    const uint64_t mask = n_bits >= 64 ? ~0ULL : ((1ULL << n_bits) - 1);
+    group_sum_kernel<<<grid_size(groups), 256, 0, (cudaStream_t)stream>>>(mask, groups, (uint32_t)g, in,
+                                                                           add, out);
     return done();
 }
 

@@ -6,8 +6,9 @@ elementwise Beaver product.
 Round budgets are the reference's: comparison 1, ReLU 2, argmax 2, maxpool 3,
 maxpool_k2 4. Every step runs on device: the masked messages are wire-packed
 kernels, evaluation is ``fss_dcf_eval`` / ``fss_dpf_eval`` and the products are
-``fss_beaver_mul``; window extraction and the small reductions are device
-tensor ops.
+``fss_beaver_mul``; the pairwise differences and the group sums of argmax /
+maxpool are ``fss_ring_pairwise`` / ``fss_ring_group_sum``; window extraction
+is a device tensor op.
 
 Beyond the reference: ``maxpool`` and ``maxpool_k2``
 also accept a batch of planes (..., m, m) and pool all of them in the same 3 /
@@ -26,7 +27,7 @@ from dataclasses import dataclass
 
 import torch
 
-from . import _dev, fss
+from . import _dev, _lib, fss
 from .beaver import BeaverTriple, mul_protocol, unroll_planes
 from .ring import RingTensor
 from .sharing import AdditiveShare
@@ -80,25 +81,31 @@ def relu_mask(session, x: AdditiveShare, cmp_keys: fss.CmpKeyBatch) -> AdditiveS
     return _plus_public(-s, 1)
 
 
-_OFF_DIAG = {}
 
 
-def _off_diagonal(m: int, device) -> torch.Tensor:
-    """Off-diagonal positions of an m x m block in row-major (j, i) order,
-    cached per device (building it per call would be a blocking H2D copy)."""
-    key = (m, str(device))
-    if key not in _OFF_DIAG:
-        idx = torch.arange(m * m, dtype=torch.int64, device=device)
-        _OFF_DIAG[key] = idx[idx // m != idx % m].contiguous()
-    return _OFF_DIAG[key]
+def _pairwise_diffs(data: torch.Tensor, m: int, n_bits: int) -> torch.Tensor:
+    """[..., j, i] = x_i - x_j mod 2^n with the diagonal removed, grouped by j
+    (nn_ops.py:111-114): (..., m*(m-1)), one fss_ring_pairwise launch."""
+    v = _dev.as_u64(data).contiguous()
+    out = torch.empty(*v.shape[:-1], m * (m - 1), dtype=torch.uint64, device=v.device)
+    with _dev.on(v.device):
+        _lib.call("fss_ring_pairwise", n_bits, v.numel() // m, m, _dev.ptr(v), _dev.ptr(out),
+                  _dev.stream_handle(v.device))
+    return out
 
 
-def _pairwise_diffs(data: torch.Tensor, m: int) -> torch.Tensor:
-    """[..., j, i] = x_i - x_j with the diagonal removed, grouped by j
-    (nn_ops.py:111-114): (..., m*(m-1))."""
-    v = _dev.as_i64(data)
-    diffs = (v[..., None, :] - v[..., :, None]).reshape(*v.shape[:-1], m * m)
-    return _dev.as_u64(diffs.index_select(-1, _off_diagonal(m, v.device)))
+def _group_sum(x: AdditiveShare, g: int, public: int = 0) -> AdditiveShare:
+    """Sums of consecutive groups of g entries along the last axis, plus a
+    public constant added by party 0 (fss_ring_group_sum): shape
+    (..., last // g)."""
+    v = _dev.as_u64(x.values.data).contiguous()
+    shape = tuple(v.shape[:-1]) + (v.shape[-1] // g,)
+    out = torch.empty(shape, dtype=torch.uint64, device=v.device)
+    add = (public if x.party == 0 else 0) & _dev.FULL64
+    with _dev.on(v.device):
+        _lib.call("fss_ring_group_sum", x.n_bits, out.numel(), g, _dev.ptr(v), add, _dev.ptr(out),
+                  _dev.stream_handle(v.device))
+    return AdditiveShare(x.party, RingTensor(out, x.n_bits, _trusted=True), x.precision)
 
 
 def argmax(session, x: AdditiveShare, prep: ArgmaxPrep) -> AdditiveShare:
@@ -106,10 +113,10 @@ def argmax(session, x: AdditiveShare, prep: ArgmaxPrep) -> AdditiveShare:
     m = x.shape[-1]
     if m < 2:
         raise ValueError("argmax needs at least two entries")
-    y = AdditiveShare(x.party, RingTensor(_pairwise_diffs(x.values.data, m), x.n_bits), 0)
+    y = AdditiveShare(x.party, RingTensor(_pairwise_diffs(x.values.data, m, x.n_bits), x.n_bits,
+                                          _trusted=True), 0)
     s = fss.sign_protocol(session, y, prep.cmp)  # 1[x_i <= x_j]
-    counts = s.reshape(*s.shape[:-1], m, m - 1).sum(axis=-1)
-    centered = _plus_public(counts, -(m - 1))
+    centered = _group_sum(s, m - 1, -(m - 1))    # per-j counts, centred by party 0
     return fss.eq_protocol(session, centered, prep.eq)
 
 
@@ -140,7 +147,7 @@ def maxpool(session, x: AdditiveShare, k: int, prep: MaxpoolPrep, stride: int = 
                                                     _trusted=True))
     onehot = argmax(session, perturbed, prep.argmax)
     prods = mul_protocol(session, onehot, wshare, prep.dot_triple)
-    pooled = prods.sum(axis=-1)
+    pooled = _group_sum(prods, kk)
     return pooled.reshape(*lead, side, side)
 
 

@@ -188,3 +188,24 @@ def test_bit_decompose_recompose(n):
                      for i in range(n)])
     assert np.array_equal(bits, want)
     assert recompose(bits, n) == A
+
+
+@pytest.mark.parametrize("n,m,lead", [(32, 4, (3, 5)), (8, 2, (7,)), (64, 9, (2, 3)), (17, 5, (1,))])
+def test_pairwise_and_group_sum_kernels_vs_numpy(n, m, lead):
+    """fss_ring_pairwise / fss_ring_group_sum against the reference's numpy
+    formulas (nn_ops.py:111-116): off-diagonal x_i - x_j grouped by j, and
+    group sums plus party 0's public constant."""
+    rng = np.random.default_rng(m * 100 + n)
+    v = rng.integers(0, np.iinfo(np.uint64).max, lead + (m,), dtype=np.uint64, endpoint=True) & _u(n)
+    with np.errstate(over="ignore"):
+        want = (v[..., None, :] - v[..., :, None])[..., ~np.eye(m, dtype=bool)] & _u(n)
+    got = nn_ops._pairwise_diffs(torch.from_numpy(v).cuda(), m, n)
+    assert got.shape == want.shape and np.array_equal(got.cpu().numpy(), want)
+    for party in (0, 1):
+        share = sharing.AdditiveShare(party, RingTensor(want, n), 0)
+        out = nn_ops._group_sum(share, m - 1, -(m - 1))
+        with np.errstate(over="ignore"):
+            ref = want.reshape(lead + (m, m - 1)).sum(axis=-1, dtype=np.uint64)
+            if party == 0:
+                ref = ref + np.uint64((-(m - 1)) & ((1 << 64) - 1))
+        assert out.shape == lead + (m,) and np.array_equal(out.values.numpy(), ref & _u(n))
