@@ -26,9 +26,11 @@ from typing import Optional
 import numpy as np
 import torch
 
-from . import _dev, _lib, _pcg, prg
+from . import _dev, _lib, _pcg, prg, ring_ops
 from ._lib import PcgState
-from .ring import ring_mask
+from .ring import RingTensor, ring_mask
+from .runtime import FRAME_MASKED
+from .sharing import AdditiveShare, _flat_u64, _pack, _peer_wire
 
 LAMBDA = prg.SEED_BITS
 
@@ -377,6 +379,7 @@ def _take_unused(batch, m: int):
     consumed[h : h+m] are all free they ARE the first m free keys and go out as
     one contiguous zero-copy slice in O(m); otherwise the full scan is used.
     The handed-out batch is spent: its mask is a read-only all-True view."""
+    _prime_ready(batch)
     if isinstance(getattr(type(batch), "consumed", None), _ConsumedMask):
         lo = _ConsumedMask.take_prefix(batch, m)
         if lo is not None:                 # O(1): no mask scan, no mask write now
@@ -683,6 +686,22 @@ def _same_key(a, b) -> bool:
     return len(a) == len(b) and all(x is y or (type(x) is not torch.Tensor and x == y) for x, y in zip(a, b))
 
 
+def _prime_ready(k):
+    """Validate a batch once before it hands out keys, so the contiguous
+    views that ``take_unused`` returns inherit the cached check (without it
+    every online call would re-validate its fresh view). Never re-lays out
+    the parent: a batch without a uniform level stride stays unprimed."""
+    if not isinstance(k, (EqKeyBatch, CmpKeyBatch)) or "_ready" in k.__dict__:
+        return
+    try:
+        k.validate()
+    except KeyFormatError:
+        return          # reported where the keys are used, as before
+    ld = _level_stride(k, _EQ_LEVEL if isinstance(k, EqKeyBatch) else _CMP_LEVEL)
+    if ld is not None:
+        k.__dict__["_ready"] = (_ready_key(k), ld)
+
+
 def _inherit_ready(parent, child, sel):
     c = parent.__dict__.get("_ready")
     if isinstance(sel, slice) and c is not None and _same_key(c[0], _ready_key(parent)):
@@ -870,9 +889,6 @@ def _masked_round(session, y, alpha_share, n: int, op: str):
     """The one online round of mask_and_reveal (sharing.py:214-230) up to the
     opening: returns this party's wire-packed m_j = y_j + alpha_j and the
     peer's. The opening x = m_0 + m_1 happens inside the evaluation kernel."""
-    from .runtime import FRAME_MASKED
-    from .sharing import _flat_u64, _pack, _peer_wire
-
     masked = _pack(0, _flat_u64(y.values), _flat_u64(alpha_share), n)
     peer = session.exchange(op, FRAME_MASKED, masked, elements=masked.numel())
     return masked, _peer_wire(peer, n, masked.numel(), masked.device)
@@ -912,10 +928,6 @@ def sign_protocol(session, y, keys: CmpKeyBatch):
 
     The masked message m_j = y_j + alpha_j is wire-packed on device, exchanged,
     and opened inside the DCF evaluation kernel (fss_dcf_eval_masked)."""
-    from .ring import RingTensor
-    from .sharing import AdditiveShare
-    from . import ring_ops
-
     m = y.values.size
     if keys.out_bits != y.values.n_bits:
         raise ValueError("key output ring does not match the shared input")
@@ -936,9 +948,6 @@ def sign_protocol(session, y, keys: CmpKeyBatch):
 
 def eq_protocol(session, y, keys: EqKeyBatch):
     """Shares of 1[y == 0] for an additively shared y. One online round, exact (fss.py:476-491)."""
-    from .ring import RingTensor
-    from .sharing import AdditiveShare
-
     m = y.values.size
     if keys.n_bits != y.values.n_bits:
         raise ValueError("key ring width does not match the shared input")

@@ -156,9 +156,11 @@ def maxpool_k2(session, x: AdditiveShare, prep: MaxpoolK2Prep) -> AdditiveShare:
     four rounds (nn_ops.py:179-190)."""
     win, lead, side = _windows(x, 2, 2)
     flat = _dev.as_i64(win.reshape(-1, 4))
-    lhs = AdditiveShare(x.party, RingTensor(_dev.as_u64(flat[:, [0, 2]].contiguous()), x.n_bits,
+    # window entries (0, 2) and (1, 3) as strided views (a Python index list
+    # would be a host-to-device copy of the list on every call)
+    lhs = AdditiveShare(x.party, RingTensor(_dev.as_u64(flat[:, 0::2].contiguous()), x.n_bits,
                                             _trusted=True), x.precision)
-    rhs = AdditiveShare(x.party, RingTensor(_dev.as_u64(flat[:, [1, 3]].contiguous()), x.n_bits,
+    rhs = AdditiveShare(x.party, RingTensor(_dev.as_u64(flat[:, 1::2].contiguous()), x.n_bits,
                                             _trusted=True), x.precision)
     mx = rhs + relu(session, lhs - rhs, prep.level1)
     m2 = _dev.as_i64(mx.values.data)

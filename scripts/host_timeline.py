@@ -2,7 +2,7 @@
 wraps the protocol's host entry points with perf_counter spans per party
 thread and prints them relative to the run start, plus the wall time.
 
-  python scripts/host_timeline.py [relu|config1|argmax]
+  python scripts/host_timeline.py [relu|config1|argmax|k2]
 """
 import functools
 import os
@@ -83,6 +83,8 @@ def once():
             preps.append(v.relu_shaped(shape))
         elif what == "config1":
             preps.append(v.cmp_keys(1 << 16))
+        elif what == "k2":
+            preps.append(v.maxpool_k2(56, planes=1024))
         else:
             preps.append(v.maxpool(56, 2, 2, planes=1024))
     torch.cuda.synchronize()
@@ -92,6 +94,8 @@ def once():
             return nn_ops.relu(s, xs[s.party], preps[s.party])
         if what == "config1":
             return fss.sign_protocol(s, AdditiveShare(s.party, xs[s.party].values, 0), preps[s.party])
+        if what == "k2":
+            return nn_ops.maxpool_k2(s, xs[s.party], preps[s.party])
         return nn_ops.maxpool(s, xs[s.party], 2, preps[s.party], 2)
     LOG.clear()
     GPU.clear()
