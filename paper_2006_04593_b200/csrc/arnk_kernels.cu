@@ -13,6 +13,7 @@
 // elements, i.e. coalesced. All byte-level (re)assembly happens in shared
 // memory, so HBM traffic is the algorithmic bytes: the payload once plus the
 // key arrays once.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -472,18 +473,55 @@ __host__ __device__ __forceinline__ Stage stage_layout(int kind, int n, uint32_t
     return g;
 }
 
+// Assemble the element-major payload records of one tile (m <= E elements)
+// from its staged level-major key rows S (layout G) into the tile buffer.
+template <int KIND, int W, int THREADS>
+__device__ __forceinline__ void assemble_stage(uint8_t* tile, const uint8_t* S, const Stage& G, int n, int lnb,
+                                               uint32_t m) {
+    constexpr uint32_t rec = KIND == 0 ? 17 : 17 + W;
+    const uint32_t E = 16u << lnb;
+    const uint32_t EB = (uint32_t)elem_bytes(KIND, n);
+    const uint32_t tail = W + 16 + n * rec;
+    const int d_lv = row_step_log2(rec), d_leaf = row_step_log2(W);
+    const uint32_t items = pair_items((uint32_t)n, lnb, d_lv);
+    for (uint32_t idx = threadIdx.x; idx < items; idx += THREADS) {
+        const Item it = pair_item(idx, lnb, d_lv);
+        if (it.row >= (uint32_t)n || it.e >= m) continue;
+        const uint32_t so = it.e * EB + W + 16 + it.row * rec;
+        const uint4 v = *reinterpret_cast<const uint4*>(S + G.scw + (it.row * E + it.e) * 16);
+        const uint32_t f = S[G.tcw + it.row * E + it.e];
+        const uint64_t sg = KIND == 1 ? *reinterpret_cast<const uint64_t*>(S + G.sig + (it.row * E + it.e) * 8)
+                                      : 0;
+        const uint32_t R[7] = {v.x, v.y, v.z, v.w, f | ((uint32_t)sg << 8), (uint32_t)(sg >> 24),
+                               (uint32_t)(sg >> 56)};
+        sput_stream<rec>(tile, so, R);
+    }
+    for (uint32_t e = threadIdx.x; e < m; e += THREADS) {
+        const uint32_t so = e * EB;
+        sput_u64<W>(tile, so, *reinterpret_cast<const uint64_t*>(S + G.alpha + e * 8));
+        sput16(tile, so + W, *reinterpret_cast<const uint4*>(S + G.seed + e * 16));
+        if (KIND == 0) sput_u64<W>(tile, so + tail, *reinterpret_cast<const uint64_t*>(S + G.cwf + e * 8));
+    }
+    if (KIND == 1) {
+        const uint32_t leaf_items = pair_items((uint32_t)n + 1, lnb, d_leaf);
+        for (uint32_t idx = threadIdx.x; idx < leaf_items; idx += THREADS) {
+            const Item it = pair_item(idx, lnb, d_leaf);
+            if (it.row > (uint32_t)n || it.e >= m) continue;
+            sput_u64<W>(tile, it.e * EB + tail + it.row * W,
+                        *reinterpret_cast<const uint64_t*>(S + G.leaf + (it.row * E + it.e) * 8));
+        }
+    }
+}
+
 template <int KIND, int W>
 __global__ void __launch_bounds__(kArnkThreads)
 arnk_pack_async_kernel(int n, uint64_t count, uint64_t ld, int lnb, uint32_t stride, uint32_t sstride,
                        int use_tma, Keys k, uint8_t* buf) {
     extern __shared__ __align__(128) uint8_t smem[];
-    constexpr uint32_t rec = KIND == 0 ? 17 : 17 + W;
     uint8_t* tiles_base = smem;                    // 2 payload buffers
     uint8_t* stage_base = smem + 2 * stride;       // 2 staging buffers
     const uint32_t E = 16u << lnb;
     const uint32_t EB = (uint32_t)elem_bytes(KIND, n);
-    const uint32_t tail = W + 16 + n * rec;
-    const int d_lv = row_step_log2(rec), d_leaf = row_step_log2(W);
     const Stage G = stage_layout(KIND, n, E);
     const uint64_t tiles = (count + E - 1) / E;
     auto tile_m = [&](uint64_t t) { return (uint32_t)(count - t * E < (uint64_t)E ? count - t * E : E); };
@@ -493,7 +531,7 @@ arnk_pack_async_kernel(int n, uint64_t count, uint64_t ld, int lnb, uint32_t str
         uint8_t* S = stage_base + b * sstride;
         const uint64_t e0 = t * E;
         const uint32_t m = tile_m(t);
-        const uint32_t q16 = m, q8 = m;                     // 16-B / 8-B pieces per row
+        const uint32_t q16 = m;                             // 16-B pieces per scw row
         // scw rows (16 B per key) and seeds
         for (uint32_t i = threadIdx.x; i < (uint32_t)n * q16; i += kArnkThreads) {
             const uint32_t row = i / q16, e = i - row * q16;
@@ -557,36 +595,128 @@ arnk_pack_async_kernel(int n, uint64_t count, uint64_t ld, int lnb, uint32_t str
         // the bulk store issued from this payload buffer two tiles ago has read it
         if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncthreads();
-        const uint32_t items = pair_items((uint32_t)n, lnb, d_lv);
-        for (uint32_t idx = threadIdx.x; idx < items; idx += kArnkThreads) {
-            const Item it = pair_item(idx, lnb, d_lv);
-            if (it.row >= (uint32_t)n || it.e >= m) continue;
-            const uint32_t so = it.e * EB + W + 16 + it.row * rec;
-            const uint4 v = *reinterpret_cast<const uint4*>(S + G.scw + (it.row * E + it.e) * 16);
-            const uint32_t f = S[G.tcw + it.row * E + it.e];
-            const uint64_t sg = KIND == 1 ? *reinterpret_cast<const uint64_t*>(S + G.sig + (it.row * E + it.e) * 8)
-                                          : 0;
-            const uint32_t R[7] = {v.x, v.y, v.z, v.w, f | ((uint32_t)sg << 8), (uint32_t)(sg >> 24),
-                                   (uint32_t)(sg >> 56)};
-            sput_stream<rec>(tile, so, R);
-        }
-        for (uint32_t e = threadIdx.x; e < m; e += kArnkThreads) {
-            const uint32_t so = e * EB;
-            sput_u64<W>(tile, so, *reinterpret_cast<const uint64_t*>(S + G.alpha + e * 8));
-            sput16(tile, so + W, *reinterpret_cast<const uint4*>(S + G.seed + e * 16));
-            if (KIND == 0) sput_u64<W>(tile, so + tail, *reinterpret_cast<const uint64_t*>(S + G.cwf + e * 8));
-        }
-        if (KIND == 1) {
-            const uint32_t leaf_items = pair_items((uint32_t)n + 1, lnb, d_leaf);
-            for (uint32_t idx = threadIdx.x; idx < leaf_items; idx += kArnkThreads) {
-                const Item it = pair_item(idx, lnb, d_leaf);
-                if (it.row > (uint32_t)n || it.e >= m) continue;
-                sput_u64<W>(tile, it.e * EB + tail + it.row * W,
-                            *reinterpret_cast<const uint64_t*>(S + G.leaf + (it.row * E + it.e) * 8));
-            }
-        }
+        assemble_stage<KIND, W, kArnkThreads>(tile, S, G, n, lnb, m);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();   // payload assembled; staging buffer cur fully read
+        if (async_io) {
+            if (threadIdx.x == 0) bulk_store(gp, tile, m * EB);
+        } else {
+            copy_range(gp, tile, (uint64_t)m * EB);
+            if (threadIdx.x == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// ---- pack with the key rows staged by TMA tensor copies -------------------
+// Each level-major key array is a 2-D tensor (rows = levels, row pitch ld
+// elements): the rows of a tile are ONE box [E elements x n rows], so a tile's
+// whole staging buffer arrives with seven cp.async.bulk.tensor copies issued
+// by one thread (completion on the buffer's mbarrier), instead of every thread
+// issuing 16-byte LDGSTS pieces (the tcw rows of a 16-key tile are 16-byte
+// pieces from n different lines: 7.3 M excess L1 wavefronts per 2^22 keys,
+// profiles/ncu_arnk_pack.json) plus the index arithmetic of the stage-in
+// loops. Elements past `count` are zero-filled by the TMA unit and skipped by
+// the assembly. The staging layout is stage_layout's, so the assembly is
+// shared with the LDGSTS kernel above. Needs ld % 16 == 0 (tcw row pitch) and
+// 16-byte aligned bases; other layouts take the kernels above.
+struct PackMaps {
+    CUtensorMap scw, tcw, sig, leaf, alpha, seed, cwf;
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_1d(void* dst, const CUtensorMap* map, int c0, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(smem_u32(bar))
+        : "memory");
+}
+
+#ifndef FSSB_ARNK_TMA_THREADS
+#define FSSB_ARNK_TMA_THREADS 512
+#endif
+
+// Staging buffers per CTA (loads run STAGES - 1 tiles ahead) and CTA size,
+// measured at n = 32 with round-robin timing (scripts/arnk_bench.py,
+// profiles/r02_arnk_tma_pack.json): cmp 3 stages (0.909 of HBM vs 0.885 with
+// 2), eq 2 stages (0.933 vs 0.824 with 3), 512 threads for both.
+#ifndef FSSB_ARNK_TMA_STAGES_CMP
+#define FSSB_ARNK_TMA_STAGES_CMP 3
+#endif
+#ifndef FSSB_ARNK_TMA_STAGES_EQ
+#define FSSB_ARNK_TMA_STAGES_EQ 2
+#endif
+
+template <int KIND, int W, int THREADS, int kTmaStages>
+__global__ void __launch_bounds__(THREADS)
+arnk_pack_tma_kernel(const __grid_constant__ PackMaps M, int n, uint64_t count, int lnb, uint32_t stride,
+                     uint32_t sstride, int use_tma_store, uint8_t* buf) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);   // full barriers of the staging buffers
+    uint8_t* tiles_base = smem + 128;                      // 2 payload buffers
+    uint8_t* stage_base = tiles_base + 2 * stride;         // kTmaStages staging buffers
+    const uint32_t E = 16u << lnb;
+    const uint32_t EB = (uint32_t)elem_bytes(KIND, n);
+    const Stage G = stage_layout(KIND, n, E);
+    const uint64_t tiles = (count + E - 1) / E;
+    auto tile_m = [&](uint64_t t) { return (uint32_t)(count - t * E < (uint64_t)E ? count - t * E : E); };
+    // box bytes of one tile (out-of-range elements are delivered as zeros and count)
+    const uint32_t tx = (uint32_t)n * E * (16 + 1) + E * (8 + 16) +
+                        (KIND == 1 ? (uint32_t)(2 * n + 1) * E * 8 : E * 8);
+    auto issue = [&](uint64_t t, int b) {   // thread 0 only
+        uint8_t* S = stage_base + b * sstride;
+        const int e0 = (int)(t * E);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bars[b])), "r"(tx)
+                     : "memory");
+        tma_load_2d(S + G.scw, &M.scw, 4 * e0, 0, &bars[b]);
+        tma_load_2d(S + G.tcw, &M.tcw, e0, 0, &bars[b]);
+        tma_load_1d(S + G.alpha, &M.alpha, e0, &bars[b]);
+        tma_load_1d(S + G.seed, &M.seed, 4 * e0, &bars[b]);
+        if (KIND == 1) {
+            tma_load_2d(S + G.sig, &M.sig, e0, 0, &bars[b]);
+            tma_load_2d(S + G.leaf, &M.leaf, e0, 0, &bars[b]);
+        } else {
+            tma_load_1d(S + G.cwf, &M.cwf, e0, &bars[b]);
+        }
+    };
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < kTmaStages; b++) mbar_init(&bars[b]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int b = 0; b + 1 < kTmaStages; b++)
+            if (blockIdx.x + (uint64_t)b * gridDim.x < tiles) issue(blockIdx.x + (uint64_t)b * gridDim.x, b);
+    }
+    __syncthreads();
+    uint32_t parity = 0;   // bit b: phase of staging buffer b's mbarrier
+    int j = 0, sb = 0;     // sb = j mod kTmaStages
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, j++, sb = sb + 1 == kTmaStages ? 0 : sb + 1) {
+        uint8_t* tile = tiles_base + (j & 1) * stride;
+        const uint8_t* S = stage_base + sb * sstride;
+        const uint32_t m = tile_m(t);
+        uint8_t* gp = buf + t * E * EB;
+        const bool async_io = use_tma_store && ((m * EB) & 15u) == 0 && ((uintptr_t)gp & 15u) == 0;
+        if (threadIdx.x == 0) {
+            // the staging buffer of tile j + kTmaStages - 1 held tile j - 1, fully
+            // read before the barrier that ended iteration j - 1
+            const uint64_t tn = t + (uint64_t)(kTmaStages - 1) * gridDim.x;
+            if (tn < tiles) issue(tn, sb == 0 ? kTmaStages - 1 : sb - 1);
+            // the bulk store issued from this payload buffer two tiles ago has read it
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        }
+        mbar_wait(&bars[sb], (parity >> sb) & 1u);
+        parity ^= 1u << sb;
+        __syncthreads();   // payload buffer j & 1 is free (thread 0's wait above)
+        assemble_stage<KIND, W, THREADS>(tile, S, G, n, lnb, m);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();   // payload assembled; staging buffer sb fully read
         if (async_io) {
             if (threadIdx.x == 0) bulk_store(gp, tile, m * EB);
         } else {
@@ -651,10 +781,106 @@ cudaError_t launch_pack_async(int n, uint64_t count, uint64_t ld, Keys k, uint8_
     return cudaGetLastError();
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda
+// link dependency); NULL when the driver does not provide it.
+#ifndef FSSB_ARNK_TMA_L2PROMO
+#define FSSB_ARNK_TMA_L2PROMO 3   // CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// rows x dim0 tensor (row pitch `pitch` bytes; rows == 0: 1-D) read in boxes of
+// box0 x rows elements
+bool encode_map(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t dim0, uint32_t rows,
+                uint64_t pitch, uint32_t box0) {
+    const cuuint64_t dims[2] = {dim0, rows ? rows : 1};
+    const cuuint64_t strides[1] = {pitch};
+    const cuuint32_t box[2] = {box0, rows ? rows : 1};
+    const cuuint32_t estr[2] = {1, 1};
+    return encode_fn()(map, dt, rows ? 2 : 1, const_cast<void*>(base), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, (CUtensorMapL2promotion)FSSB_ARNK_TMA_L2PROMO,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+#ifndef FSSB_ARNK_TMA_PACK
+#define FSSB_ARNK_TMA_PACK 1
+#endif
+#ifndef FSSB_ARNK_TMA_LNB
+#define FSSB_ARNK_TMA_LNB 0
+#endif
+
+// The TMA-staged pack when the layout allows it (returns false otherwise and
+// launches nothing): tcw row pitch ld a multiple of 16 bytes, sigma / leaf
+// pitch (8 ld) too, every base 16-byte aligned, 4 count within a tensor
+// dimension.
+template <int KIND, int W>
+bool try_pack_tma(int n, uint64_t count, uint64_t ld, const Keys& k, uint8_t* buf, cudaStream_t st,
+                  cudaError_t* err) {
+    if (!FSSB_ARNK_TMA_PACK || ld % 16 || 4 * count >= (1ull << 32) || !encode_fn()) return false;
+    const uintptr_t bases = (uintptr_t)k.scw | (uintptr_t)k.tcw | (uintptr_t)k.seed0 | (uintptr_t)k.alpha_share |
+                            (uintptr_t)(KIND == 1 ? ((uintptr_t)k.sigma_cw | (uintptr_t)k.leaf_cw)
+                                                  : (uintptr_t)k.cw_final);
+    if (bases & 15) return false;
+    const int lnb = FSSB_ARNK_TMA_LNB;
+    const uint32_t E = 16u << lnb;
+    PackMaps M;
+    memset(&M, 0, sizeof(M));
+    bool ok = encode_map(&M.scw, CU_TENSOR_MAP_DATA_TYPE_UINT32, k.scw, 4 * count, n, 16 * ld, 4 * E) &&
+              encode_map(&M.tcw, CU_TENSOR_MAP_DATA_TYPE_UINT8, k.tcw, count, n, ld, E) &&
+              encode_map(&M.alpha, CU_TENSOR_MAP_DATA_TYPE_UINT64, k.alpha_share, count, 0, 8, E) &&
+              encode_map(&M.seed, CU_TENSOR_MAP_DATA_TYPE_UINT32, k.seed0, 4 * count, 0, 16, 4 * E);
+    if (KIND == 1)
+        ok = ok && encode_map(&M.sig, CU_TENSOR_MAP_DATA_TYPE_UINT64, k.sigma_cw, count, n, 8 * ld, E) &&
+             encode_map(&M.leaf, CU_TENSOR_MAP_DATA_TYPE_UINT64, k.leaf_cw, count, n + 1, 8 * ld, E);
+    else
+        ok = ok && encode_map(&M.cwf, CU_TENSOR_MAP_DATA_TYPE_UINT64, k.cw_final, count, 0, 8, E);
+    if (!ok) return false;
+    const uint32_t stride = (uint32_t)((elem_bytes(KIND, n) * E + 16 + 127) / 128 * 128);
+    const uint32_t sstride = stage_layout(KIND, n, E).bytes;
+    constexpr int kStages = KIND == 1 ? FSSB_ARNK_TMA_STAGES_CMP : FSSB_ARNK_TMA_STAGES_EQ;
+    const size_t smem = 128 + 2 * (size_t)stride + kStages * (size_t)sstride;
+    if (smem > 220 * 1024) return false;
+    constexpr int kThr = FSSB_ARNK_TMA_THREADS;
+    auto kern = arnk_pack_tma_kernel<KIND, W, kThr, kStages>;
+    int dev = 0, sms = 0, per_sm = 1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThr, smem);
+    if (e == cudaSuccess) {
+        const uint64_t tiles = (count + E - 1) / E;
+        const uint64_t cap = (uint64_t)sms * (per_sm > 0 ? per_sm : 1);
+        static const int use_tma = getenv("FSSB_ARNK_NO_TMA") ? 0 : 1;
+        kern<<<(unsigned)(tiles < cap ? tiles : cap), kThr, smem, st>>>(M, n, count, lnb, stride, sstride, use_tma,
+                                                                         buf);
+        e = cudaGetLastError();
+    }
+    *err = e;
+    return true;
+}
+
 template <bool PACK, int KIND, int W>
 cudaError_t launch_tile(int n, uint64_t count, uint64_t ld, Keys k, uint8_t* buf, cudaStream_t st) {
     // cp.async needs naturally aligned pieces: tcw rows 4-byte aligned, scw /
     // seed rows 16-byte aligned (sigma / leaf pick 16 or 8 in the kernel)
+    if (PACK) {
+        cudaError_t e = cudaSuccess;
+        if (try_pack_tma<KIND, W>(n, count, ld, k, buf, st, &e)) return e;
+    }
     if (PACK && FSSB_ARNK_ASYNC_PACK && ld % 4 == 0 && !((uintptr_t)k.tcw & 3) &&
         !(((uintptr_t)k.scw | (uintptr_t)k.seed0) & 15) && !((uintptr_t)k.alpha_share & 7) &&
         2 * (elem_bytes(KIND, n) * 16 + 144) + 2 * stage_layout(KIND, n, 16).bytes <= 220 * 1024)

@@ -21,12 +21,20 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "build", "variants")
+ROUNDS = int(os.environ.get("ARNK_ROUNDS", "6"))
 # variant name -> compile-time defines (the shipped library is "main")
 VARIANTS = {
     "naive": ["FSSB_ARNK_NAIVE=1"],
-    "unpack512": ["FSSB_ARNK_UNPACK_THREADS=512"],
-    "unpack512_e32": ["FSSB_ARNK_UNPACK_THREADS=512", "FSSB_ARNK_UNPACK_TILE_KB=100"],
+    # r02 pack study: the LDGSTS-staged kernel (shipped before the TMA tensor-map pack),
+    # TMA staging depth / CTA size / L2 promotion of the tensor maps
+    "ldgsts": ["FSSB_ARNK_TMA_PACK=0"],
+    "cmp_s2": ["FSSB_ARNK_TMA_STAGES_CMP=2"],
+    "eq_s3": ["FSSB_ARNK_TMA_STAGES_EQ=3"],
+    "tma256": ["FSSB_ARNK_TMA_THREADS=256"],
+    "promo0": ["FSSB_ARNK_TMA_L2PROMO=0"],
 }
+if os.environ.get("ARNK_VARIANTS"):
+    VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["ARNK_VARIANTS"].split(",")}
 
 
 def vlib(name):
@@ -84,6 +92,7 @@ def run(log2n: int):
                     _dev.ptr(src.get("leaf_cw"))]
 
         src = {f: getattr(k0, f) for f in fields}
+        fns = {}
         for libname, lib in libs.items():
             def pack(lib=lib, libname=libname):
                 assert lib.fss_arnk_pack(kind, 32, N, N, *ptrs(src), _dev.ptr(bufs[libname]),
@@ -92,22 +101,33 @@ def run(log2n: int):
             def unpack(lib=lib, libname=libname):
                 assert lib.fss_arnk_unpack(kind, 32, N, N, _dev.ptr(bufs[libname]), *ptrs(outs[libname]),
                                            stream.cuda_stream) == 0
+            fns[libname] = {"pack": pack, "unpack": unpack}
+            pack()
+            unpack()
+        # round-robin over the libraries (ROUNDS x 5 launches each) so clock /
+        # thermal drift hits every variant alike; median over all launches
+        times = {ln: {"pack": [], "unpack": []} for ln in libs}
+        for _ in range(ROUNDS):
+            for libname in libs:
+                for op in ("pack", "unpack"):
+                    for _ in range(5):
+                        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        a.record(stream)
+                        fns[libname][op]()
+                        b.record(stream)
+                        b.synchronize()
+                        times[libname][op].append(a.elapsed_time(b) / 1e3)
+        for libname in libs:
             row = {}
-            for op, fn in (("pack", pack), ("unpack", unpack)):
-                fn()
-                ts = []
-                for _ in range(7):
-                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    a.record(stream)
-                    fn()
-                    b.record(stream)
-                    b.synchronize()
-                    ts.append(a.elapsed_time(b) / 1e3)
-                t = sorted(ts)[len(ts) // 2]
+            for op in ("pack", "unpack"):
+                ts = sorted(times[libname][op])
+                t = ts[len(ts) // 2]
                 row[op] = {"ms": t * 1e3, "keys_per_s": N / t, "gb_per_s": N * algo / t / 1e9,
-                           "frac_hbm": N * algo / t / 1e9 / hbm}
+                           "frac_hbm": N * algo / t / 1e9 / hbm, "launches": len(ts)}
             out[f"{name}_{libname}"] = row
-            print(name, libname, json.dumps(row), flush=True)
+            print(name, libname, "pack %.4f ms frac %.4f | unpack %.4f ms frac %.4f" % (
+                row["pack"]["ms"], row["pack"]["frac_hbm"], row["unpack"]["ms"], row["unpack"]["frac_hbm"]),
+                flush=True)
         for libname in libs:
             assert torch.equal(bufs["main"], bufs[libname]), ("pack payloads differ", libname)
             for f in fields:

@@ -173,3 +173,47 @@ def test_save_packed_keys(tmp_path, kind, n, count):
     assert b.read_bytes() == a.read_bytes()
     with pytest.raises(TypeError):
         keyfile.save_keys(b, object(), object())
+
+
+def _np_payload(k, kind, n):
+    """Element-major ARNK records restated in numpy (reference LAYOUT.md:48-71,
+    fss.py:540-602): alpha[w] | seed0[16] | n x (scw[16] | flags[1] | sigma[w] (cmp))
+    | cw_final[w] (eq) / (n + 1) x leaf[w] (cmp), little-endian ring values."""
+    w = (n + 7) // 8
+    cnt = k.count
+
+    def le(v):   # (cnt,) or (rows, cnt) u64 -> (..., cnt, w) bytes
+        a = np.ascontiguousarray(v.cpu().numpy().astype(np.uint64))
+        return a.view(np.uint8).reshape(a.shape + (8,))[..., :w]
+
+    cols = [le(k.alpha_share), k.seed0.cpu().numpy().reshape(cnt, 16)]
+    scw = k.scw.cpu().numpy().reshape(n, cnt, 16)
+    tcw = k.tcw.cpu().numpy().reshape(n, cnt, 1)
+    lv = [scw, tcw] + ([le(k.sigma_cw)] if kind == "cmp" else [])
+    cols.append(np.concatenate(lv, axis=2).transpose(1, 0, 2).reshape(cnt, -1))
+    if kind == "cmp":
+        cols.append(le(k.leaf_cw).transpose(1, 0, 2).reshape(cnt, -1))
+    else:
+        cols.append(le(k.cw_final))
+    return np.concatenate(cols, axis=1)
+
+
+@pytest.mark.parametrize("kind,n,count", [("cmp", 32, 1024), ("cmp", 32, 4096), ("eq", 32, 2048),
+                                          ("cmp", 12, 512), ("eq", 7, 320), ("cmp", 63, 64),
+                                          ("eq", 64, 96), ("cmp", 4, 48)])
+def test_pack_tensor_map_path_matches_numpy(kind, n, count):
+    """Level strides that are multiples of 16 take the TMA tensor-map pack
+    (arnk_pack_tma_kernel): whole batches, prefixes with a ragged last tile
+    (zero-filled out-of-range box elements), views at 16-aligned offsets, and
+    (fallback) odd offsets -- every payload equals the numpy restatement of
+    the record layout."""
+    keygen = fss.keygen_cmp if kind == "cmp" else fss.keygen_eq
+    _, k0, _ = keygen(n, np.random.default_rng(count + n), count, device=DEV)
+    for lo, hi in ((0, count), (0, count - 1), (0, count - 15), (16, count), (32, count - 7),
+                   (16, 17), (48, 64), (1, count)):
+        hi = min(hi, count)
+        if hi <= lo:
+            continue
+        v = k0.take(slice(lo, hi))
+        got = fss._pack_device(v).cpu().numpy()
+        assert np.array_equal(got, _np_payload(v, kind, n)), (lo, hi)
