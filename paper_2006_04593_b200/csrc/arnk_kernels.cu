@@ -826,11 +826,14 @@ bool encode_map(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint
 // The TMA-staged pack when the layout allows it (returns false otherwise and
 // launches nothing): tcw row pitch ld a multiple of 16 bytes, sigma / leaf
 // pitch (8 ld) too, every base 16-byte aligned, 4 count within a tensor
-// dimension.
+// dimension, and an even count: the TMA unit moves the inner dimension in
+// 16-byte units, so a tensor of u64 values must end on a 16-byte boundary
+// (measured on the store side, r02r: an odd-count 1-D u64 tensor got one
+// element written past its end; the load side reads the same units).
 template <int KIND, int W>
 bool try_pack_tma(int n, uint64_t count, uint64_t ld, const Keys& k, uint8_t* buf, cudaStream_t st,
                   cudaError_t* err) {
-    if (!FSSB_ARNK_TMA_PACK || ld % 16 || 4 * count >= (1ull << 32) || !encode_fn()) return false;
+    if (!FSSB_ARNK_TMA_PACK || ld % 16 || count % 2 || 4 * count >= (1ull << 32) || !encode_fn()) return false;
     const uintptr_t bases = (uintptr_t)k.scw | (uintptr_t)k.tcw | (uintptr_t)k.seed0 | (uintptr_t)k.alpha_share |
                             (uintptr_t)(KIND == 1 ? ((uintptr_t)k.sigma_cw | (uintptr_t)k.leaf_cw)
                                                   : (uintptr_t)k.cw_final);

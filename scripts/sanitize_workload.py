@@ -26,6 +26,14 @@ for n, N in ((32, 3000), (12, 513), (63, 77)):
     q0, q1 = k0.take(slice(0, N - 2)), k1.take(slice(0, N - 2))
     fss.unpack_keys(fss.deserialize_keys(fss.serialize_keys(fss.pack_keys(q0, q1))))
 fss.keygen_eq(64, rng, 100)
+# ARNK pack through TMA tensor maps (level stride a multiple of 16): whole
+# batches, ragged prefixes (zero-filled box elements), 16-aligned views
+for n, N in ((32, 3008), (12, 512), (63, 64)):
+    a, k0, k1 = fss.keygen_cmp(n, rng, N)
+    a, e0, e1 = fss.keygen_eq(n, rng, N)
+    for lo, hi in ((0, N), (0, N - 5), (16, N - 3)):
+        fss._pack_device(k0.take(slice(lo, hi)))
+        fss._pack_device(e0.take(slice(lo, hi)))
 # sharded dealer (tape slices) and streaming key files
 for r in range(3):
     shard.keygen_cmp_shard(32, np.random.default_rng(4), 1001, r, 3)

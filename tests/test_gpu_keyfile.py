@@ -202,18 +202,69 @@ def _np_payload(k, kind, n):
                                           ("cmp", 12, 512), ("eq", 7, 320), ("cmp", 63, 64),
                                           ("eq", 64, 96), ("cmp", 4, 48)])
 def test_pack_tensor_map_path_matches_numpy(kind, n, count):
-    """Level strides that are multiples of 16 take the TMA tensor-map pack
-    (arnk_pack_tma_kernel): whole batches, prefixes with a ragged last tile
-    (zero-filled out-of-range box elements), views at 16-aligned offsets, and
-    (fallback) odd offsets -- every payload equals the numpy restatement of
-    the record layout."""
+    """Level strides that are multiples of 16 and even counts take the TMA
+    tensor-map pack (arnk_pack_tma_kernel): whole batches, prefixes with a
+    ragged last tile (zero-filled out-of-range box elements), views at
+    16-aligned offsets; odd counts and odd offsets take the fallbacks -- every
+    payload equals the numpy restatement of the record layout."""
     keygen = fss.keygen_cmp if kind == "cmp" else fss.keygen_eq
     _, k0, _ = keygen(n, np.random.default_rng(count + n), count, device=DEV)
-    for lo, hi in ((0, count), (0, count - 1), (0, count - 15), (16, count), (32, count - 7),
-                   (16, 17), (48, 64), (1, count)):
+    for lo, hi in ((0, count), (0, count - 1), (0, count - 6), (0, count - 15), (16, count), (32, count - 7),
+                   (32, count - 2), (16, 17), (16, 18), (48, 64), (1, count)):
         hi = min(hi, count)
         if hi <= lo:
             continue
         v = k0.take(slice(lo, hi))
         got = fss._pack_device(v).cpu().numpy()
         assert np.array_equal(got, _np_payload(v, kind, n)), (lo, hi)
+
+
+@pytest.mark.parametrize("kind,n,count", [("cmp", 32, 1024), ("eq", 32, 2048), ("cmp", 12, 512),
+                                          ("eq", 7, 320), ("cmp", 63, 64), ("eq", 64, 96)])
+def test_unpack_into_column_range(kind, n, count):
+    """Unpack into fresh arrays and into a column range of padded arrays
+    (ld > count, 16-aligned and unaligned column offsets, ragged last tiles):
+    the keys come back exactly and no byte outside the range changes (a TMA
+    tensor-store unpack was measured and dropped in r02: slower, and its
+    16-byte clipping wrote past an odd-count u64 column range)."""
+    from paper_2006_04593_b200 import _dev, _lib
+    keygen = fss.keygen_cmp if kind == "cmp" else fss.keygen_eq
+    kid = fss.KIND_CMP if kind == "cmp" else fss.KIND_EQ
+    _, k0, _ = keygen(n, np.random.default_rng(count + 7 * n), count, device=DEV)
+    for lo, hi in ((0, count), (16, count), (0, count - 5), (32, count - 3), (16, 17)):
+        v = k0.take(slice(lo, hi))
+        m = hi - lo
+        payload = fss._pack_device(v).reshape(-1)
+        _same(fss._unpack(kid, 0, n, m, payload, DEV), v)
+        for c0 in (16, 3):
+            L = (c0 + m + 40) // 16 * 16
+
+            def arr(*shape, dt=torch.uint8):
+                return torch.full(shape, 0xAB, dtype=torch.uint8, device=DEV).view(dt) if dt != torch.uint8 \
+                    else torch.full(shape, 0xAB, dtype=torch.uint8, device=DEV)
+            full = {"alpha_share": arr(L, 8, dt=torch.uint64).reshape(L), "seed0": arr(L, 16),
+                    "scw": arr(n, L, 16), "tcw": arr(n, L)}
+            if kind == "cmp":
+                full["sigma_cw"] = arr(n, L, 8, dt=torch.uint64).reshape(n, L)
+                full["leaf_cw"] = arr(n + 1, L, 8, dt=torch.uint64).reshape(n + 1, L)
+            else:
+                full["cw_final"] = arr(L, 8, dt=torch.uint64).reshape(L)
+            before = {f: t.clone() for f, t in full.items()}
+            col = {f: (t[c0:c0 + m] if t.dim() == 1 or f == "seed0" else t[:, c0:c0 + m]) for f, t in full.items()}
+            rc = _lib.call("fss_arnk_unpack", kid, n, m, L, _dev.ptr(payload), _dev.ptr(col["alpha_share"]),
+                           _dev.ptr(col["seed0"]), _dev.ptr(col["scw"]), _dev.ptr(col["tcw"]),
+                           _dev.ptr(col.get("cw_final")), _dev.ptr(col.get("sigma_cw")),
+                           _dev.ptr(col.get("leaf_cw")), _dev.stream_handle(DEV))
+            assert rc in (0, None)
+            torch.cuda.synchronize()
+
+            def b(t):   # u8 view, element axis kept (u64 -> trailing 8-byte axis)
+                return t.contiguous().view(torch.uint8).reshape(*t.shape, -1) if t.dtype != torch.uint8 else t
+            for f, t in full.items():
+                exp = b(before[f]).clone()
+                src = b(getattr(v, f).contiguous())
+                if t.dim() == 1 or f == "seed0":
+                    exp[c0:c0 + m] = src
+                else:
+                    exp[:, c0:c0 + m] = src
+                assert torch.equal(b(t), exp), (f, lo, hi, c0)
