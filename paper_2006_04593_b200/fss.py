@@ -116,6 +116,41 @@ def _check_party_tensors(k, names):
             raise KeyFormatError(f"{name} lives on {t.device}, expected {dev}")
 
 
+# Lazy slices: take_unused's O(1) hand-out of keys [lo, lo + m) of a batch
+# whose arrays passed the eval layout check records (parent arrays, lo, m,
+# level stride) instead of building six tensor views (~3.5 us of host time
+# each, on the critical path of every online protocol). A field is created as
+# a view of the parent's array when it is first read (cached per batch, so the
+# same tensor object is returned on every read); the evaluation entry points
+# take the device pointers straight from the parent arrays while no field of
+# the batch has been assigned.
+_LAZY_ROWS = ("scw", "tcw", "sigma_cw", "leaf_cw")   # level-major: element axis 1
+
+
+def _lazy_field(obj, name):
+    d = obj.__dict__
+    lz = d.get("_lazy")
+    if lz is None or name not in lz[0]:
+        raise AttributeError(f"{type(obj).__name__!r} object has no attribute {name!r}")
+    cache = d.setdefault("_lazyv", {})
+    v = cache.get(name)
+    if v is None:
+        t, lo, m = lz[0][name], lz[1], lz[2]
+        v = t[:, lo:lo + m] if name in _LAZY_ROWS else t[lo:lo + m]
+        cache[name] = v
+    return v
+
+
+def _lazy_ptrs(k, names):
+    """(parent arrays, lo, count, ld) of a lazy slice none of whose `names`
+    fields was assigned, else None."""
+    d = k.__dict__
+    lz = d.get("_lazy")
+    if lz is None or any(n in d for n in names):
+        return None
+    return lz
+
+
 class _ConsumedMask:
     """The ``consumed`` field of the key batches (reference fss.py:92-102): a
     host numpy bool mask, as in the reference -- with the single-use hand-out
@@ -185,11 +220,16 @@ class EqKeyBatch:
 
     @property
     def count(self) -> int:
-        return int(self.alpha_share.shape[0])
+        lz = self.__dict__.get("_lazy")
+        return lz[2] if lz is not None else int(self.alpha_share.shape[0])
 
     @property
     def device(self):
-        return self.alpha_share.device
+        lz = self.__dict__.get("_lazy")
+        return (lz[0]["alpha_share"] if lz is not None else self.alpha_share).device
+
+    def __getattr__(self, name):   # reached only for names missing from __dict__
+        return _lazy_field(self, name)
 
     def validate(self):
         n, count = self.n_bits, self.count
@@ -233,11 +273,16 @@ class CmpKeyBatch:
 
     @property
     def count(self) -> int:
-        return int(self.alpha_share.shape[0])
+        lz = self.__dict__.get("_lazy")
+        return lz[2] if lz is not None else int(self.alpha_share.shape[0])
 
     @property
     def device(self):
-        return self.alpha_share.device
+        lz = self.__dict__.get("_lazy")
+        return (lz[0]["alpha_share"] if lz is not None else self.alpha_share).device
+
+    def __getattr__(self, name):   # reached only for names missing from __dict__
+        return _lazy_field(self, name)
 
     def validate(self):
         n, count = self.n_bits, self.count
@@ -359,6 +404,30 @@ def _eval_packed(party: int, k: PackedKeyBatch, x, out, m_own=None, m_peer=None)
 _SPENT = np.ones(0, dtype=bool)
 
 
+def _lazy_slice(batch, lo: int, m: int):
+    """The lazy form of batch.take(slice(lo, lo + m)) for a spent hand-out, or
+    None when the batch is not a ready level-major batch with contiguous
+    per-element arrays (the caller then takes the eager views)."""
+    if m == 0 or type(batch) not in (EqKeyBatch, CmpKeyBatch):
+        return None
+    d = batch.__dict__
+    c = d.get("_ready")
+    if c is None or "_lazy" in d or not _same_key(c[0], _ready_key(batch)):
+        return None
+    names = _LAZY_NAMES[type(batch)]
+    P = {n: d[n] for n in names}
+    if not (P["alpha_share"].is_contiguous() and P["seed0"].is_contiguous()
+            and ("cw_final" not in P or P["cw_final"].is_contiguous())):
+        return None
+    child = object.__new__(type(batch))
+    cd = child.__dict__
+    cd.update(party=batch.party, n_bits=batch.n_bits, _lazy=(P, lo, m, c[1]))
+    if type(batch) is CmpKeyBatch:
+        cd["out_bits"] = batch.out_bits
+    cd.update(_cons=_spent(m), _pend=[], _front=None)   # the consumed field: all spent
+    return child
+
+
 def _spent(m: int) -> np.ndarray:
     """A read-only all-True mask of m keys: the ``consumed`` field of a batch
     handed out by take_unused (every key of it is spent). One shared buffer,
@@ -384,6 +453,9 @@ def _take_unused(batch, m: int):
         lo = _ConsumedMask.take_prefix(batch, m)
         if lo is not None:                 # O(1): no mask scan, no mask write now
             batch._free_hint = lo + m
+            lazy = _lazy_slice(batch, lo, m)
+            if lazy is not None:
+                return lazy
             return batch.take(slice(lo, lo + m), _consumed=_spent(m))
     consumed = batch.consumed
     count = consumed.shape[0]
@@ -534,7 +606,7 @@ def _keygen_eq_core(n: int, alpha, alpha0, s0_init, s1_init):
                   _dev.ptr(alpha1), _dev.stream_handle(dev))
     k0 = EqKeyBatch(0, n, alpha0, s0_init, scw, tcw, cw_final)
     k1 = EqKeyBatch(1, n, alpha1, s1_init, scw, tcw, cw_final)
-    return k0, k1
+    return _born_ready(k0, count), _born_ready(k1, count)
 
 
 def _keygen_cmp_core(n: int, alpha, alpha0, s0_init, s1_init, out_bits: int = None):
@@ -555,7 +627,7 @@ def _keygen_cmp_core(n: int, alpha, alpha0, s0_init, s1_init, out_bits: int = No
                   _dev.ptr(sigma_cw), _dev.ptr(leaf_cw), _dev.ptr(alpha1), _dev.stream_handle(dev))
     k0 = CmpKeyBatch(0, n, alpha0, s0_init, scw, tcw, sigma_cw, leaf_cw, out_bits=out_bits)
     k1 = CmpKeyBatch(1, n, alpha1, s1_init, scw, tcw, sigma_cw, leaf_cw, out_bits=out_bits)
-    return k0, k1
+    return _born_ready(k0, count), _born_ready(k1, count)
 
 
 def keygen_eq(n: int, rng: np.random.Generator, count: int = 1,
@@ -656,6 +728,8 @@ def _eval_operands(k, names):
 
 _EQ_LEVEL = ("tcw",)
 _CMP_LEVEL = ("tcw", "sigma_cw", "leaf_cw")
+_LAZY_NAMES = {EqKeyBatch: ("alpha_share", "seed0", "scw", "tcw", "cw_final"),
+               CmpKeyBatch: ("alpha_share", "seed0", "scw", "tcw", "sigma_cw", "leaf_cw")}
 
 
 def _ready_key(k):
@@ -673,6 +747,10 @@ def _ready(k, names) -> int:
     on the batch while its arrays stay the same objects; a contiguous take()
     of a ready batch inherits it (column views keep the level stride), so the
     batches take_unused hands to the online protocols skip both."""
+    names_all = _LAZY_NAMES.get(type(k))
+    lz = _lazy_ptrs(k, names_all) if names_all else None
+    if lz is not None:      # an unassigned take_unused slice: the parent's check holds
+        return lz[3]
     c = k.__dict__.get("_ready")
     if c is not None and _same_key(c[0], _ready_key(k)):
         return c[1]
@@ -700,6 +778,16 @@ def _prime_ready(k):
     ld = _level_stride(k, _EQ_LEVEL if isinstance(k, EqKeyBatch) else _CMP_LEVEL)
     if ld is not None:
         k.__dict__["_ready"] = (_ready_key(k), ld)
+
+
+def _born_ready(k, count: int):
+    """Mark a batch that keygen just built from fresh contiguous arrays of the
+    validated shapes as checked, level stride = count (what validate() and the
+    stride probe would find): the first take_unused of the online phase then
+    skips both."""
+    if "_ready" not in k.__dict__:
+        k.__dict__["_ready"] = (_ready_key(k), max(count, 1))
+    return k
 
 
 def _inherit_ready(parent, child, sel):
@@ -897,28 +985,41 @@ def _masked_round(session, y, alpha_share, n: int, op: str):
 def _eval_cmp_masked(party: int, k: CmpKeyBatch, m_own, m_peer) -> torch.Tensor:
     if isinstance(k, PackedKeyBatch):
         return _eval_packed(party, k, None, None, m_own, m_peer)
-    ld = _ready(k, _CMP_LEVEL)
-    dev = k.device
-    seed0 = k.seed0.contiguous()
-    out = torch.empty(k.count, dtype=torch.uint64, device=dev)
+    lz = _lazy_ptrs(k, ("seed0", "scw", "tcw", "sigma_cw", "leaf_cw"))
+    if lz is not None:      # a take_unused slice: pointers into the parent's arrays
+        P, lo, count, ld = lz
+        dev = P["scw"].device
+        ptrs = (P["seed0"].data_ptr() + 16 * lo, P["scw"].data_ptr() + 16 * lo, P["tcw"].data_ptr() + lo,
+                P["sigma_cw"].data_ptr() + 8 * lo, P["leaf_cw"].data_ptr() + 8 * lo)
+    else:
+        ld = _ready(k, _CMP_LEVEL)
+        dev, count = k.device, k.count
+        ptrs = (_dev.ptr(k.seed0.contiguous()), _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(k.sigma_cw),
+                _dev.ptr(k.leaf_cw))
+    out = torch.empty(count, dtype=torch.uint64, device=dev)
     with _dev.on(dev):
-        _lib.call("fss_dcf_eval_masked", int(party), k.n_bits, int(k.out_bits), k.count, ld,
-                  _dev.ptr(seed0), _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(k.sigma_cw),
-                  _dev.ptr(k.leaf_cw), _dev.ptr(m_own), _dev.ptr(m_peer), _dev.ptr(out),
-                  _dev.stream_handle(dev))
+        _lib.call("fss_dcf_eval_masked", int(party), k.n_bits, int(k.out_bits), count, ld, *ptrs,
+                  _dev.ptr(m_own), _dev.ptr(m_peer), _dev.ptr(out), _dev.stream_handle(dev))
     return out
 
 
 def _eval_eq_masked(party: int, k: EqKeyBatch, m_own, m_peer) -> torch.Tensor:
     if isinstance(k, PackedKeyBatch):
         return _eval_packed(party, k, None, None, m_own, m_peer)
-    ld = _ready(k, _EQ_LEVEL)
-    dev = k.device
-    seed0, cw_final = k.seed0.contiguous(), k.cw_final.contiguous()
-    out = torch.empty(k.count, dtype=torch.uint64, device=dev)
+    lz = _lazy_ptrs(k, ("seed0", "scw", "tcw", "cw_final"))
+    if lz is not None:      # a take_unused slice: pointers into the parent's arrays
+        P, lo, count, ld = lz
+        dev = P["scw"].device
+        ptrs = (P["seed0"].data_ptr() + 16 * lo, P["scw"].data_ptr() + 16 * lo, P["tcw"].data_ptr() + lo,
+                P["cw_final"].data_ptr() + 8 * lo)
+    else:
+        ld = _ready(k, _EQ_LEVEL)
+        dev, count = k.device, k.count
+        ptrs = (_dev.ptr(k.seed0.contiguous()), _dev.ptr(k.scw), _dev.ptr(k.tcw),
+                _dev.ptr(k.cw_final.contiguous()))
+    out = torch.empty(count, dtype=torch.uint64, device=dev)
     with _dev.on(dev):
-        _lib.call("fss_dpf_eval_masked", int(party), k.n_bits, k.count, ld, _dev.ptr(seed0),
-                  _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(cw_final), _dev.ptr(m_own),
+        _lib.call("fss_dpf_eval_masked", int(party), k.n_bits, count, ld, *ptrs, _dev.ptr(m_own),
                   _dev.ptr(m_peer), _dev.ptr(out), _dev.stream_handle(dev))
     return out
 

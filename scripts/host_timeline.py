@@ -51,6 +51,13 @@ for mod, names in ((fss, ["sign_protocol", "eq_protocol", "_masked_round", "_eva
                    (beaver, ["beaver_protocol"]), (nn_ops, ["relu", "argmax", "maxpool"])):
     for n in names:
         wrap(mod, n, f"{mod.__name__.split('.')[-1]}.{n}")
+if os.environ.get("FINE"):   # finer host spans of the prologue up to the first evaluation launch
+    for mod, names in ((nn_ops, ["_plus_public", "mul_protocol"]), (fss, ["_pack", "_peer_wire"]),
+                       (runtime, ["run_session"])):
+        for n in names:
+            if hasattr(mod, n):
+                wrap(mod, n, f"{mod.__name__.split('.')[-1]}.{n}")
+    wrap(fss.CmpKeyBatch, "take_unused", "CmpKeyBatch.take_unused")
 _orig_ex = runtime.Session.exchange
 
 

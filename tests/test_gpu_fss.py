@@ -426,9 +426,12 @@ def test_ready_cache_follows_the_arrays():
     x = alpha.clone()
     y = fss.eval_cmp(0, k0, x)
     assert "_ready" in k0.__dict__
-    sub = k0.take_unused(40)
-    assert "_ready" in sub.__dict__ and sub.__dict__["_ready"][1] == 64      # parent's level stride
+    sub = k0.take_unused(40)                 # a lazy slice: the parent's arrays, check and stride
+    assert "_lazy" in sub.__dict__ and fss._ready(sub, fss._CMP_LEVEL) == 64
     assert torch.equal(fss.eval_cmp(0, sub, x[:40]).view(torch.int64), y[:40].view(torch.int64))
+    view = k0.take(slice(40, 64))
+    assert "_ready" in view.__dict__ and view.__dict__["_ready"][1] == 64    # parent's level stride
+    assert torch.equal(fss.eval_cmp(0, view, x[40:]).view(torch.int64), y[40:].view(torch.int64))
     gathered = k0.take(np.array([5, 1, 60]))                                # gather: no inheritance
     assert "_ready" not in gathered.__dict__
     pick = torch.tensor([5, 1, 60], device=x.device)
