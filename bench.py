@@ -406,8 +406,13 @@ def measure_pair_protocol(dev, xdev, rank, barrier, max_over_ranks, M=1 << 22, r
     for name, make in (("nccl", lambda: runtime.DistTransport(peer, device=xdev)),
                        ("peer_memory", lambda: runtime.PeerTransport(peer, device=dev,
                                                                      capacity=8 * M))):
+        try:
+            transport = make()
+        except runtime.PeerAccessError as e:     # raised on both ranks of the pair alike
+            out[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+            continue
         keys = dealer.make_dealer(32, seed=77 + pair).for_party(party).cmp_keys(M * (reps + 1))
-        sess = runtime.Session(party, make())
+        sess = runtime.Session(party, transport)
         fss.sign_protocol(sess, y, keys)          # warm-up
         barrier()
         torch.cuda.synchronize()
@@ -443,7 +448,11 @@ def measure_gather(k0, k1, x, total, rank, barrier, max_over_ranks, reps=5):
         y0, y1 = eval_only()
         return shard.gather_ring(y0, N_BITS, total, dst=0), shard.gather_ring(y1, N_BITS, total, dst=0)
 
-    g = shard.PeerGather(total, slots=2, dst=0)
+    from paper_2006_04593_b200.runtime import PeerAccessError
+    try:
+        g = shard.PeerGather(total, slots=2, dst=0)
+    except PeerAccessError as e:                 # agreed over all ranks: all skip it
+        g, peer_error = None, f"{type(e).__name__}: {e}"[:300]
 
     def fused():
         fss.eval_cmp(0, k0, x, out=g.out(0))
@@ -456,11 +465,17 @@ def measure_gather(k0, k1, x, total, rank, barrier, max_over_ranks, reps=5):
             assert bool(((rec == 0) | (rec == 1)).all()), "gathered shares do not reconstruct to bits"
 
     check(*nccl())
-    res = fused()
-    if rank == 0:
-        check(res[0], res[1])
+    if g is not None:
+        res = fused()
+        if rank == 0:
+            check(res[0], res[1])
     out = {"elements": total, "bytes_to_rank0_wire": 2 * total * 4, "bytes_to_rank0_fused": 2 * total * 8}
-    for name, fn in (("eval_only", eval_only), ("nccl_gather", nccl), ("peer_fused", fused)):
+    variants = [("eval_only", eval_only), ("nccl_gather", nccl)]
+    if g is not None:
+        variants.append(("peer_fused", fused))
+    else:
+        out["peer_fused_error"] = peer_error
+    for name, fn in variants:
         fn()
         barrier()
         torch.cuda.synchronize()
@@ -469,7 +484,8 @@ def measure_gather(k0, k1, x, total, rank, barrier, max_over_ranks, reps=5):
             fn()
         torch.cuda.synchronize()
         out[f"{name}_ms_per_step"] = max_over_ranks((time.perf_counter() - t0) / reps) * 1e3
-    g.close()
+    if g is not None:
+        g.close()
     return out
 
 

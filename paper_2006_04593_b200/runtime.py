@@ -51,6 +51,12 @@ class SessionAbort(RuntimeError):
     """Protocol aborted: peer failure, timeout, or frame desync (runtime.py:40-41)."""
 
 
+class PeerAccessError(SessionAbort):
+    """CUDA IPC mapping of the peer's buffers failed (no peer access between the
+    two GPUs, or IPC unavailable). Raised on BOTH ranks: the mapping outcome is
+    agreed before any peer load or store."""
+
+
 @dataclass
 class Frame:
     """One message: a tag and a device (or host) tensor payload."""
@@ -449,21 +455,40 @@ class PeerTransport:
         cap = max(int(nbytes), 1 << 12)
         hb = lib.load().fss_ipc_handle_bytes()
         mine = torch.zeros((2, hb), dtype=torch.uint8)
+        err = None
         with torch.cuda.device(self.device):
-            for i in range(2):
-                ptr = ctypes.c_void_p()
-                lib.call("fss_ipc_alloc", cap, ctypes.byref(ptr))
-                self._slots.append(ptr.value)
-                buf = (ctypes.c_uint8 * hb)()
-                lib.call("fss_ipc_get_handle", ptr, buf)
-                mine[i] = torch.tensor(list(buf), dtype=torch.uint8)
+            try:
+                for i in range(2):
+                    ptr = ctypes.c_void_p()
+                    lib.call("fss_ipc_alloc", cap, ctypes.byref(ptr))
+                    self._slots.append(ptr.value)
+                    buf = (ctypes.c_uint8 * hb)()
+                    lib.call("fss_ipc_get_handle", ptr, buf)
+                    mine[i] = torch.tensor(list(buf), dtype=torch.uint8)
+            except RuntimeError as e:           # still swap (zeros), then agree below
+                err = e
         theirs = self._swap(mine)
         with torch.cuda.device(self.device):
-            for i in range(2):
-                raw = (ctypes.c_uint8 * hb)(*theirs[i].tolist())
-                ptr = ctypes.c_void_p()
-                lib.call("fss_ipc_open_handle", raw, ctypes.byref(ptr))
-                self._peer_ptrs.append(ptr.value)
+            try:
+                for i in range(2):
+                    if err is not None or bool(theirs[i].eq(0).all()):
+                        err = err or "the peer exported no buffer"
+                        break
+                    raw = (ctypes.c_uint8 * hb)(*theirs[i].tolist())
+                    ptr = ctypes.c_void_p()
+                    lib.call("fss_ipc_open_handle", raw, ctypes.byref(ptr))
+                    self._peer_ptrs.append(ptr.value)
+            except RuntimeError as e:
+                err = e
+        # both sides learn whether both mappings exist before either uses one, so
+        # a failed mapping fails the two parties alike (no side left blocked in
+        # a later exchange waiting for a peer that raised)
+        ok = self._swap(torch.tensor([0 if err else 1], dtype=torch.int64))
+        if err is not None or int(ok[0]) != 1:
+            self._release()
+            self._closed = True
+            raise PeerAccessError("peer memory mapping failed on "
+                                  + (f"this rank: {err}" if err else "the peer"))
         self._cap = cap
 
     def _release(self):

@@ -171,21 +171,46 @@ class PeerGather:
         hb = _lib.load().fss_ipc_handle_bytes()
         handle = torch.zeros(hb, dtype=torch.uint8)
         self._owned = None
+        err, opened = None, False
         with _dev.on(self.device):
             if self.rank == self.dst:
                 ptr = ctypes.c_void_p()
-                _lib.call("fss_ipc_alloc", max(8 * self.slots * self.total, 16), ctypes.byref(ptr))
-                self._owned = self.base = ptr.value
-                buf = (ctypes.c_uint8 * hb)()
-                _lib.call("fss_ipc_get_handle", ptr, buf)
-                handle = torch.tensor(list(buf), dtype=torch.uint8)
-            comm = handle.to(self.device) if dist.get_backend(group) == "nccl" else handle
+                try:
+                    _lib.call("fss_ipc_alloc", max(8 * self.slots * self.total, 16), ctypes.byref(ptr))
+                    self._owned = self.base = ptr.value
+                    buf = (ctypes.c_uint8 * hb)()
+                    _lib.call("fss_ipc_get_handle", ptr, buf)
+                    handle = torch.tensor(list(buf), dtype=torch.uint8)
+                except RuntimeError as e:      # still broadcast (zeros), then agree below
+                    err = e
+            nccl = dist.get_backend(group) == "nccl"
+            comm = handle.to(self.device) if nccl else handle
             dist.broadcast(comm, src=self.dst, group=group)
             if self.rank != self.dst:
-                raw = (ctypes.c_uint8 * hb)(*comm.cpu().tolist())
-                ptr = ctypes.c_void_p()
-                _lib.call("fss_ipc_open_handle", raw, ctypes.byref(ptr))
-                self.base = ptr.value
+                if bool(comm.eq(0).all()):
+                    err = "the destination rank exported no buffer"
+                else:
+                    raw = (ctypes.c_uint8 * hb)(*comm.cpu().tolist())
+                    ptr = ctypes.c_void_p()
+                    try:
+                        _lib.call("fss_ipc_open_handle", raw, ctypes.byref(ptr))
+                        self.base, opened = ptr.value, True
+                    except RuntimeError as e:
+                        err = e
+            # every rank learns whether every mapping exists before any store:
+            # a rank failing alone would leave the others in finish()'s barrier
+            ok = torch.tensor([0 if err else 1], dtype=torch.int64,
+                              device=self.device if nccl else "cpu")
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+            if int(ok.item()) != 1:
+                if self._owned is not None:
+                    _lib.call("fss_ipc_free", ctypes.c_void_p(self._owned))
+                elif opened:
+                    _lib.call("fss_ipc_close_handle", ctypes.c_void_p(self.base))
+                self._closed = True
+                from .runtime import PeerAccessError
+                raise PeerAccessError("PeerGather: peer memory mapping failed on "
+                                      + (f"this rank: {err}" if err else "another rank"))
         self._closed = False
 
     def out(self, slot: int):
