@@ -394,9 +394,9 @@ def _eval_packed(party: int, k: PackedKeyBatch, x, out, m_own=None, m_peer=None)
     out = _check_out(out, count, dev)
     xt, host = _prep_x(x, count, n, dev)
 
-    def launch(lo, hi, xd, od, stream):
+    def launch(xd, od, stream):
         with _dev.on(dev):
-            _lib.call(fn, int(party), n, hi - lo, _dev.ptr(k.payload[lo:hi]), _dev.ptr(xd), None, None,
+            _lib.call(fn, int(party), n, count, _dev.ptr(k.payload), _dev.ptr(xd), None, None,
                       _dev.ptr(od), stream)
     return _run_eval(launch, xt, host, count, dev, None, out)
 
@@ -821,7 +821,7 @@ def _check_out(out, count: int, dev):
 def _run_eval(launch, xt, host, count: int, dev, host_launch=None, out=None):
     """Run the evaluation over [0, count).
 
-    Device input: ``launch(lo, hi, x_dev, out_dev, stream)`` once on the current
+    Device input: ``launch(x_dev, out_dev, stream)`` once on the current
     stream. Pinned host torch input: the same launch on the host pointers
     (zero-copy) into a pinned host result. numpy input (pageable) of at least
     PIPELINE_MIN elements: ``host_launch(x_ptr, out_ptr, x_scratch, out_scratch,
@@ -833,7 +833,7 @@ def _run_eval(launch, xt, host, count: int, dev, host_launch=None, out=None):
     if out is not None:
         if host:
             raise ValueError("out= needs a device input x (device in, device out)")
-        launch(0, count, xt, out, _dev.stream_handle(dev))
+        launch(xt, out, _dev.stream_handle(dev))
         return out
     if host == "torch_pinned":
         # Zero-copy: the evaluation kernel reads x straight from the caller's
@@ -844,14 +844,14 @@ def _run_eval(launch, xt, host, count: int, dev, host_launch=None, out=None):
         # 2^24 DCF keys 4.42e8 vs 4.28e8 comparisons/s through the pipeline,
         # 2^20 keys 4.24e8 vs 3.35e8 (scripts/zerocopy_probe.py).
         out_host = torch.empty(count, dtype=torch.uint64, pin_memory=True)
-        launch(0, count, xt, out_host, _dev.stream_handle(dev))
+        launch(xt, out_host, _dev.stream_handle(dev))
         torch.cuda.current_stream(dev).synchronize()
         return out_host
     if not big or host != "numpy":
         if host == "numpy":
             xt = torch.from_numpy(xt).to(dev, non_blocking=True)
         out = torch.empty(count, dtype=torch.uint64, device=dev)
-        launch(0, count, xt, out, _dev.stream_handle(dev))
+        launch(xt, out, _dev.stream_handle(dev))
         return _result(out, {"numpy": True}.get(host, host))
     chunk = PIPELINE_CHUNK
     cur = torch.cuda.current_stream(dev)
@@ -874,6 +874,9 @@ def _run_eval(launch, xt, host, count: int, dev, host_launch=None, out=None):
 def _prep_x(x, count: int, n: int, dev):
     """_broadcast_x plus the host fast paths (no upload here; the kernels reduce
     x mod 2^n themselves)."""
+    if isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.uint64 \
+            and x.numel() == count and x.device == dev and x.is_contiguous():
+        return x.view(-1), False           # the online protocols' case: nothing to convert
     if isinstance(x, torch.Tensor) and not x.is_cuda and x.is_pinned() and x.is_contiguous() \
             and x.numel() == count and x.dtype in (torch.uint64, torch.int64):
         # contiguous pinned memory only: the zero-copy kernel reads it in place
@@ -896,11 +899,10 @@ def eval_eq(party: int, k: EqKeyBatch, x, out=None):
     xt, host = _prep_x(x, count, n, dev)
     seed0, cw_final = k.seed0.contiguous(), k.cw_final.contiguous()
 
-    def launch(lo, hi, xd, od, stream):
+    def launch(xd, od, stream):   # whole batch: no column views to build
         with _dev.on(dev):
-            _lib.call("fss_dpf_eval", int(party), n, hi - lo, ld, _dev.ptr(seed0[lo:hi]),
-                      _dev.ptr(k.scw[:, lo:hi]), _dev.ptr(k.tcw[:, lo:hi]),
-                      _dev.ptr(cw_final[lo:hi]), _dev.ptr(xd), _dev.ptr(od), stream)
+            _lib.call("fss_dpf_eval", int(party), n, count, ld, _dev.ptr(seed0), _dev.ptr(k.scw),
+                      _dev.ptr(k.tcw), _dev.ptr(cw_final), _dev.ptr(xd), _dev.ptr(od), stream)
 
     def host_launch(xh, oh, xs, os_, chunk, stage, sa, sb):
         with _dev.on(dev):
@@ -943,12 +945,11 @@ def eval_cmp(party: int, k: CmpKeyBatch, x, return_levels: bool = False, out=Non
                       _dev.ptr(xt), _dev.ptr(out), _dev.ptr(levels), _dev.stream_handle(dev))
         return _result(out, host), _result(levels, host)
 
-    def launch(lo, hi, xd, od, stream):
+    def launch(xd, od, stream):   # whole batch: no column views to build
         with _dev.on(dev):
-            _lib.call("fss_dcf_eval", int(party), n, int(k.out_bits), hi - lo, ld,
-                      _dev.ptr(seed0[lo:hi]), _dev.ptr(k.scw[:, lo:hi]), _dev.ptr(k.tcw[:, lo:hi]),
-                      _dev.ptr(k.sigma_cw[:, lo:hi]), _dev.ptr(k.leaf_cw[:, lo:hi]), _dev.ptr(xd),
-                      _dev.ptr(od), None, stream)
+            _lib.call("fss_dcf_eval", int(party), n, int(k.out_bits), count, ld, _dev.ptr(seed0),
+                      _dev.ptr(k.scw), _dev.ptr(k.tcw), _dev.ptr(k.sigma_cw), _dev.ptr(k.leaf_cw),
+                      _dev.ptr(xd), _dev.ptr(od), None, stream)
 
     def host_launch(xh, oh, xs, os_, chunk, stage, sa, sb):
         with _dev.on(dev):
