@@ -62,6 +62,8 @@ __device__ __forceinline__ void fill_tables(uint32_t* tab) {
 #ifndef FSSB_TMA_TABLES
 #define FSSB_TMA_TABLES 1
 #endif
+// (static: one image per translation unit; fss_kernels.cu is the only unit
+// that launches table kernels, and its prep_launch uploads its image)
 static __device__ __align__(128) uint32_t g_tab_img[kTableWords];
 
 __device__ __forceinline__ void load_tables(uint32_t* tab) {
@@ -108,6 +110,11 @@ inline cudaError_t table_image_upload() {
     }
     err = cudaMemcpyToSymbol(g_tab_img, img, sizeof(uint32_t) * kTableWords);
     delete[] img;
+    // From pageable memory the copy returns once the bytes are staged, not
+    // when they reach HBM, and the legacy stream it ran on does not order the
+    // party / torch streams (non-blocking): wait for it before any kernel that
+    // pulls the image can be launched.
+    if (err == cudaSuccess) err = cudaStreamSynchronize(cudaStreamLegacy);
     return err;
 }
 
