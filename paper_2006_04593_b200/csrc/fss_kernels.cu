@@ -37,10 +37,10 @@ namespace {
 // AES): +0.7 % for DCF eval at 1024 threads, -1.4 % for DPF eval
 // (profiles/r01_aes_variants_c.json), so on for DCF only.
 #ifndef FSSB_PREFETCH_DCF
-#define FSSB_PREFETCH_DCF 1
+#define FSSB_PREFETCH_DCF 1   // levels ahead (0: no prefetch)
 #endif
 #ifndef FSSB_PREFETCH_DPF
-#define FSSB_PREFETCH_DPF 0
+#define FSSB_PREFETCH_DPF 0   // levels ahead (0: no prefetch)
 #endif
 #ifdef FSSB_PREFETCH
 #undef FSSB_PREFETCH_DCF
@@ -67,6 +67,19 @@ namespace {
 // Eval kernels: 32 warps per SM (64 registers) hide the LDS / LDG latency best
 // (profiles/r01_aes_variants_b.json: 512 -> 1024 threads = +5 % DCF, +17 % DPF).
 constexpr int kThreads = FSSB_THREADS;
+constexpr int kPfDcf = FSSB_PREFETCH_DCF;
+constexpr int kPfDpf = FSSB_PREFETCH_DPF;
+struct DpfCw {
+    U4 s;
+    uint32_t f;
+};
+// One level's DCF correction words as one thread reads them.
+template <typename W>
+struct DcfCw {
+    U4 s;          // seed correction
+    uint32_t f;    // tL, tR, tauL, tauR bits
+    W sig, leaf;
+};
 // Keygen kernels need ~100-127 registers: 16 warps per SM.
 constexpr int kKeygenThreads = 512;
 
@@ -168,7 +181,6 @@ dpf_eval_kernel(int party, int n, uint64_t count, uint64_t ld, const uint8_t* __
                 const uint64_t* __restrict__ cw_final, const uint64_t* __restrict__ x,
                 const void* __restrict__ m_own, const void* __restrict__ m_peer,
                 uint64_t* __restrict__ out) {
-    constexpr bool PF = FSSB_PREFETCH_DPF;
     extern __shared__ __align__(128) uint32_t tab[];
     fssb::load_tables(tab);
     const fssb::Tab tb = fssb::make_tab(tab);
@@ -178,32 +190,31 @@ dpf_eval_kernel(int party, int n, uint64_t count, uint64_t ld, const uint8_t* __
         U4 s = ld16(seed0 + 16 * e);
         uint32_t t = party;
         const uint64_t xe = load_x(x, m_own, m_peer, n, e) & mask;
-        // software pipeline: level i+1's correction words load during level i's AES
-        U4 cw = PF ? ld16(scw + 16 * e) : U4{0, 0, 0, 0};
-        uint32_t f = PF ? __ldg(tcw + e) : 0u;
+        auto cw_at = [&](int i) {
+            const uint64_t off = (uint64_t)(i < n ? i : n - 1) * ld + e;
+            return DpfCw{ld16(scw + 16 * off), __ldg(tcw + off)};
+        };
+        // kPfDpf levels of correction words in flight (see dcf_eval_kernel)
+        DpfCw ring[kPfDpf > 0 ? kPfDpf : 1];
+#pragma unroll
+        for (int j = 0; j < kPfDpf; j++) ring[j] = cw_at(j);
         for (int i = 0; i < n; i++) {
-            U4 cw_next;
-            uint32_t f_next;
-            if (PF) {
-                const uint64_t offn = (uint64_t)(i + 1 < n ? i + 1 : i) * ld + e;
-                cw_next = ld16(scw + 16 * offn);
-                f_next = __ldg(tcw + offn);
+            DpfCw c;
+            if (kPfDpf > 0) {
+                c = ring[0];
+#pragma unroll
+                for (int j = 0; j + 1 < kPfDpf; j++) ring[j] = ring[j + 1];
+                ring[kPfDpf > 0 ? kPfDpf - 1 : 0] = cw_at(i + kPfDpf);
             } else {
-                const uint64_t off = (uint64_t)i * ld + e;
-                cw = ld16(scw + 16 * off);
-                f = __ldg(tcw + off);
+                c = cw_at(i);
             }
             const uint32_t xb = (uint32_t)(xe >> (n - 1 - i)) & 1u;
             const U4 a = fssb::mmo<0, true>(tb, s, 0u - xb);
             const uint32_t tm = 0u - t;
-            s = xor4(a, and4(cw, tm));
-            const uint32_t tn = ((a.w >> 31) ^ (t & (f >> xb))) & 1u;
+            s = xor4(a, and4(c.s, tm));
+            const uint32_t tn = ((a.w >> 31) ^ (t & (c.f >> xb))) & 1u;
             s.w &= 0x7FFFFFFFu;
             t = tn;
-            if (PF) {
-                cw = cw_next;
-                f = f_next;
-            }
         }
         uint64_t o = (((uint64_t)t * cw_final[e]) + lo64(s)) & mask;
         if (party) o = (0 - o) & mask;
@@ -247,27 +258,33 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
         uint32_t t = party;
         W acc = 0;
         const uint64_t xe = load_x(x, m_own, m_peer, n, e) & nmask;
-#if FSSB_PREFETCH_DCF
-        U4 cw = ld16(scw + 16 * e);
-        uint32_t f = __ldg(tcw + e);
-        W sig = __ldg(sig_w + kStride * e);
-        W leaf = __ldg(leaf_w + kStride * e);
-#endif
+        // correction words of level i (clamped to the last level, so the
+        // prefetch ring never reads past the arrays)
+        auto cw_at = [&](int i) {
+            const uint64_t off = (uint64_t)(i < n ? i : n - 1) * ld + e;
+            return DcfCw<W>{ld16(scw + 16 * off), __ldg(tcw + off), __ldg(sig_w + kStride * off),
+                            __ldg(leaf_w + kStride * off)};
+        };
+        // software pipeline, kPfDcf levels deep: ptxas schedules a load late in
+        // the iteration that issues it, so distance 1 covers only the tail of one
+        // level's AES; distance 0 loads each level's words where they are used
+        DcfCw<W> ring[kPfDcf > 0 ? kPfDcf : 1];
+#pragma unroll
+        for (int j = 0; j < kPfDcf; j++) ring[j] = cw_at(j);
 #pragma unroll kDcfUnroll
         for (int i = 0; i < n; i++) {
-#if FSSB_PREFETCH_DCF
-            const uint64_t offn = (uint64_t)(i + 1 < n ? i + 1 : i) * ld + e;
-            const U4 cw_next = ld16(scw + 16 * offn);
-            const uint32_t f_next = __ldg(tcw + offn);
-            const W sig_next = __ldg(sig_w + kStride * offn);
-            const W leaf_next = __ldg(leaf_w + kStride * offn);
-#else
-            const uint64_t off = (uint64_t)i * ld + e;
-            const U4 cw = ld16(scw + 16 * off);
-            const uint32_t f = __ldg(tcw + off);
-            const W sig = __ldg(sig_w + kStride * off);
-            const W leaf = __ldg(leaf_w + kStride * off);
-#endif
+            DcfCw<W> c;
+            if (kPfDcf > 0) {
+                c = ring[0];
+#pragma unroll
+                for (int j = 0; j + 1 < kPfDcf; j++) ring[j] = ring[j + 1];
+                ring[kPfDcf > 0 ? kPfDcf - 1 : 0] = cw_at(i + kPfDcf);
+            } else {
+                c = cw_at(i);
+            }
+            const U4 cw = c.s;
+            const uint32_t f = c.f;
+            const W sig = c.sig, leaf = c.leaf;
             const uint32_t xb = (uint32_t)(xe >> (n - 1 - i)) & 1u;
             const uint32_t tm = 0u - t;
             // sigma/tau lane x_i of the third block (slice_cmp, prg.py:99-119):
@@ -287,12 +304,6 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
             const uint32_t tn = ((a.w >> 31) ^ (t & (f >> xb))) & 1u;
             s.w &= 0x7FFFFFFFu;
             t = tn;
-#if FSSB_PREFETCH_DCF
-            cw = cw_next;
-            f = f_next;
-            sig = sig_next;
-            leaf = leaf_next;
-#endif
         }
         const uint64_t off = (uint64_t)n * ld + e;
         const W lo = W32 ? (W)s.x : (W)lo64(s);
