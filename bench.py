@@ -728,6 +728,9 @@ def run_strong(args, ctx):
         "keygen": ({"pairs_per_s": total * args.steps / t_kg, "ms_per_step": t_kg / args.steps * 1e3}
                    if t_kg else None),
         "wall_ms_per_step_incl_keygen": wall / args.steps * 1e3,
+        "wall_note": ("host wall clock per step: every chunk's keygen, its device-x eval of both "
+                      "parties (the timed value) and, unless --no-e2e, the same eval again from "
+                      "pinned host x (e2e)"),
         **roofline_blocks(int(n_avg), avg_launch_s, peaks_live, hbm_peak, hbm_src,
                           load_traffic(), f"2^{int(np.log2(n_avg))}"),
         "peaks_probe": peaks_live,
