@@ -488,15 +488,20 @@ def _device_tape_ok(n: int, rng) -> bool:
     return 1 <= n <= 63 and _pcg.is_pcg64(rng)
 
 
-def _sample_tape(n: int, rng, count: int, alpha, device, shard=None):
+def _sample_tape(n: int, rng, count: int, alpha, device, shard=None, defer=None):
     """fss._sample_tape (fss.py:292-303): draw order alpha (unless given),
     alpha0, s0, s1 -- bit-identical to the reference's numpy draws.
 
     ``shard=(lo, m)`` materialises only the element slice [lo, lo + m) of the
     ``count``-element tape (a given ``alpha`` is then the slice's, shape (m,));
-    ``rng`` still advances past the whole tape (see shard.py)."""
+    ``rng`` still advances past the whole tape (see shard.py).
+
+    ``defer`` (a list): on the device-tape paths the advance of ``rng`` (a
+    128-bit LCG jump in Python, ~15 us) is appended as a callable instead of
+    run, so keygen can launch its kernel first and advance the generator while
+    the GPU works; the caller runs it before returning."""
     if shard is not None:
-        return _sample_tape_slice(n, rng, count, alpha, device, *shard)
+        return _sample_tape_slice(n, rng, count, alpha, device, *shard, defer=defer)
     if alpha is not None:
         alpha_t = _dev.to_device_u64(alpha, device)
         if tuple(alpha_t.shape) != (count,):
@@ -533,11 +538,18 @@ def _sample_tape(n: int, rng, count: int, alpha, device, shard=None):
         _lib.call("fss_pcg64_tape", cst, n, count, int(draw_alpha),
                   _dev.ptr(a) if draw_alpha else None, _dev.ptr(a0), _dev.ptr(s0), _dev.ptr(s1),
                   out_st, _dev.stream_handle(device))
-    _pcg.commit(rng, st, out_st, count > 0)   # advance the caller's rng exactly as numpy would
+    _commit(rng, st, out_st, count > 0, defer)   # advance the caller's rng exactly as numpy would
     return a, a0, s0, s1
 
 
-def _sample_tape_slice(n: int, rng, count: int, alpha, device, lo: int, m: int):
+def _commit(rng, st, out_st, drawn: bool, defer):
+    if defer is None:
+        _pcg.commit(rng, st, out_st, drawn)
+    else:
+        defer.append(lambda: _pcg.commit(rng, st, out_st, drawn))
+
+
+def _sample_tape_slice(n: int, rng, count: int, alpha, device, lo: int, m: int, defer=None):
     if not (0 <= lo and 0 <= m and lo + m <= count):
         raise ValueError(f"tape slice [{lo}, {lo + m}) outside a tape of {count}")
     alpha_t = None
@@ -566,7 +578,7 @@ def _sample_tape_slice(n: int, rng, count: int, alpha, device, lo: int, m: int):
         _lib.call("fss_pcg64_tape_slice", cst, n, count, lo, m, int(draw_alpha),
                   _dev.ptr(a) if draw_alpha else None, _dev.ptr(a0), _dev.ptr(s0), _dev.ptr(s1),
                   out_st, _dev.stream_handle(device))
-    _pcg.commit(rng, st, out_st, count > 0)   # the generator moves past the WHOLE tape
+    _commit(rng, st, out_st, count > 0, defer)   # the generator moves past the WHOLE tape
     return a, a0, s0, s1
 
 
@@ -637,8 +649,13 @@ def keygen_eq(n: int, rng: np.random.Generator, count: int = 1,
     if not 4 <= n <= 64:
         raise ValueError("equality keys support 4 <= n <= 64")
     dev = _dev.default_device(device)
-    a, a0, s0, s1 = _sample_tape(n, rng, count, alpha, dev, _shard)
-    k0, k1 = _keygen_eq_core(n, a, a0, s0, s1)
+    pending = []
+    try:
+        a, a0, s0, s1 = _sample_tape(n, rng, count, alpha, dev, _shard, pending)
+        k0, k1 = _keygen_eq_core(n, a, a0, s0, s1)
+    finally:
+        for advance in pending:   # the generator moves while the keygen kernel runs
+            advance()
     return a, k0, k1
 
 
@@ -656,8 +673,13 @@ def keygen_cmp(n: int, rng: np.random.Generator, count: int = 1,
     if out_bits is not None and not n <= out_bits <= 63:
         raise ValueError("out_bits must lie in [n, 63]")
     dev = _dev.default_device(device)
-    a, a0, s0, s1 = _sample_tape(n, rng, count, alpha, dev, _shard)
-    k0, k1 = _keygen_cmp_core(n, a, a0, s0, s1, out_bits)
+    pending = []
+    try:
+        a, a0, s0, s1 = _sample_tape(n, rng, count, alpha, dev, _shard, pending)
+        k0, k1 = _keygen_cmp_core(n, a, a0, s0, s1, out_bits)
+    finally:
+        for advance in pending:   # the generator moves while the keygen kernel runs
+            advance()
     return a, k0, k1
 
 
