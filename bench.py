@@ -60,9 +60,11 @@ N_BITS = 32
 BYTES_PER_EVAL = 16 + 32 * 16 + 32 + 32 * 8 + 33 * 8 + 8 + 8   # 1096 B
 AES_PER_EVAL = 64                                              # 32 levels x 2 blocks
 LDS_PER_AES = 160                                              # T-table lookups per block
-# Lookups the T-table DCF evaluation needs per party-eval: per level one full
-# block (160) + the sigma half-block (144 rounds 1-9 + 8 last-round) = 312.
-LOOKUPS_PER_EVAL = 32 * (160 + 152)                            # 9,984
+# Lookups the T-table DCF evaluation needs per party-eval at out_bits <= 32 (the
+# bench's ring): per level one full block (160) + the sigma block's rounds 1-9
+# (144) + its last-round bytes that the output reads (4 for sigma mod 2^32, 1
+# for the tau bit) = 309.
+LOOKUPS_PER_EVAL = 32 * (160 + 149)                            # 9,888
 # one conflict-free LDS.32 wavefront serves 32 lanes' lookups
 LOP3_PER_AES_BITSLICED = 356.25                                # SURVEY.md §8d bitsliced floor
 
@@ -539,7 +541,8 @@ def roofline_blocks(N: int, avg_launch_s: float, peaks_live: dict, hbm_peak: flo
                                  "bound this kernel (DESIGN.md section 3)"),
                      "aes_blocks_per_s": aes_rate,
                      "note": (f"{LOOKUPS_PER_EVAL} algorithmic lookups per party-eval (32 levels x "
-                              "[160 for the child block + 152 for the sigma half-block]) x "
+                              "[160 for the child block + 149 for the sigma block: rounds 1-9 and the 5 "
+                              "last-round bytes that sigma mod 2^32 and tau read]) x "
                               f"{label} party-evals per launch / CUDA-event launch time; "
                               "peak = 32 x the measured conflict-free LDS wavefront rate on this GPU "
                               f"({peaks_live['lds_wavefronts_per_s']:.4g}/s, fss_probe_peaks); "

@@ -245,7 +245,11 @@ __device__ __forceinline__ U4 aes128(const Tab& tb, U4 s, uint32_t m) {
 // 1: bytes 8..15; hm = 0 - h). The last round then needs 8 of the 16 lookups:
 // DCF evaluation reads only the sigma/tau lane x_i of the third block
 // (slice_cmp, prg.py:99-119), so this is exact. Returns (lo, hi) words.
-template <int KEY>
+// TOP_HI: the caller uses only bit 31 of `hi` (the tau bit; sigma mod 2^w with
+// w <= 32 lives in `lo`), so the high word's last round is the one lookup that
+// yields its top byte: 5 last-round lookups instead of 8. The other bits of
+// `hi` are then not the block's.
+template <int KEY, bool TOP_HI = false>
 __device__ __forceinline__ void mmo_half(const Tab& tb, U4 s, uint32_t hm, uint32_t& lo,
                                          uint32_t& hi) {
     uint32_t c0 = s.x, c1 = s.y, c2 = s.z, c3 = s.w;
@@ -256,7 +260,9 @@ __device__ __forceinline__ void mmo_half(const Tab& tb, U4 s, uint32_t hm, uint3
     const uint32_t k_hi = kRK[KEY][41] ^ (hm & (kRK[KEY][41] ^ kRK[KEY][43]));
     const uint32_t s_lo = hm ? s.z : s.x, s_hi = hm ? s.w : s.y;
     lo = lop3_xor3(last_col(tb, a0, a1, a2, a3), k_lo, s_lo);
-    hi = lop3_xor3(last_col(tb, a1, a2, a3, a0), k_hi, s_hi);
+    // byte 3 of last_col(a1, a2, a3, a0) is byte 3 of T<1,3>(a0): S(a0.b3)
+    hi = TOP_HI ? lop3_xor3(T<1, 3>(tb, a0), k_hi, s_hi)
+                : lop3_xor3(last_col(tb, a1, a2, a3, a0), k_hi, s_hi);
 }
 
 // Matyas-Meyer-Oseas block: AES_k(s) XOR s  (reference prg.expand, prg.py:43-60).

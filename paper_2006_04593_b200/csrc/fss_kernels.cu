@@ -291,7 +291,8 @@ dcf_eval_kernel(int party, int n, int out_bits, uint64_t count, uint64_t ld,
             // only that 8-byte half of AES_k3(s) ^ s is computed
             uint32_t lane_lo, lane_hi;
             const U4 a = fssb::mmo<0, true>(tb, s, 0u - xb);
-            fssb::mmo_half<2>(tb, s, 0u - xb, lane_lo, lane_hi);
+            // W32: sigma is lane_lo mod 2^w, and only the tau bit of lane_hi is read
+            fssb::mmo_half<2, W32>(tb, s, 0u - xb, lane_lo, lane_hi);
             W lane;
             if (W32) lane = (W)lane_lo;
             else lane = (W)(((uint64_t)lane_hi << 32) | lane_lo);
@@ -423,7 +424,8 @@ dcf_eval_packed_kernel(int party, int n, uint64_t count, const uint8_t* __restri
             const U4 a = fssb::mmo<0, true>(tb, s, 0u - xb);
             const uint32_t tm = 0u - t;
             uint32_t lane_lo, lane_hi;
-            fssb::mmo_half<2>(tb, s, 0u - xb, lane_lo, lane_hi);
+            // n <= 32: the ring sum mod 2^n never sees lane_hi beyond its tau bit
+            fssb::mmo_half<2, (W <= 4)>(tb, s, 0u - xb, lane_lo, lane_hi);
             const uint64_t lane = ((uint64_t)lane_hi << 32) | lane_lo;
             const uint32_t tau = ((lane_hi >> 31) ^ (t & (f >> (2 + xb)))) & 1u;
             const uint64_t sigma = lane ^ (sig & (0 - (uint64_t)t));

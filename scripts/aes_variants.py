@@ -74,8 +74,8 @@ def run(log2n: int):
             assert rc == 0
 
         row = {}
-        # lookups per party-eval: DCF 32 x (160 + 152: sigma half-block), DPF 32 x 160
-        for kname, fn, ref, aes, lk in (("dcf_eval", dcf, ref0, 64, 9984),
+        # lookups per party-eval: DCF 32 x (160 + 149: sigma block at out_bits <= 32), DPF 32 x 160
+        for kname, fn, ref, aes, lk in (("dcf_eval", dcf, ref0, 64, 9888),
                                         ("dpf_eval", dpf, ref_e, 32, 5120)):
             fn()
             torch.cuda.synchronize()
