@@ -265,6 +265,23 @@ __device__ __forceinline__ void mmo_half(const Tab& tb, U4 s, uint32_t hm, uint3
                 : lop3_xor3(last_col(tb, a1, a2, a3, a0), k_hi, s_hi);
 }
 
+// MMO block AES_KEY(s) ^ s for DCF keygen's sigma/tau block at out_bits <= 32:
+// the correction words read sigma_L / sigma_R mod 2^w (words x and z) and the
+// tau bits (bit 31 of words y and w), so words y and w get only the last-round
+// lookup of their top byte -- 10 of the 16 last-round lookups. Bits 0..30 of
+// y and w are then not the block's.
+template <int KEY>
+__device__ __forceinline__ U4 mmo_sigma_tau32(const Tab& tb, U4 s) {
+    uint32_t c0 = s.x, c1 = s.y, c2 = s.z, c3 = s.w;
+    aes128_rounds<KEY, false>(tb, c0, c1, c2, c3, 0);
+    U4 o;
+    o.x = lop3_xor3(last_col(tb, c0, c1, c2, c3), kRK[KEY][40], s.x);
+    o.y = lop3_xor3(T<1, 3>(tb, c0), kRK[KEY][41], s.y);   // byte 3 of last_col(c1, c2, c3, c0)
+    o.z = lop3_xor3(last_col(tb, c2, c3, c0, c1), kRK[KEY][42], s.z);
+    o.w = lop3_xor3(T<1, 3>(tb, c2), kRK[KEY][43], s.w);   // byte 3 of last_col(c3, c0, c1, c2)
+    return o;
+}
+
 // Matyas-Meyer-Oseas block: AES_k(s) XOR s  (reference prg.expand, prg.py:43-60).
 template <int KEY, bool SEL>
 __device__ __forceinline__ U4 mmo(const Tab& tb, U4 s, uint32_t m) {

@@ -593,7 +593,8 @@ dcf_keygen_kernel(int n, int out_bits, uint64_t count, const uint64_t* __restric
 // seed / t corrections, the odd lane sigma and the leaf word.
 constexpr int kPairKeygenThreads = 1024;
 
-template <bool CMP>
+// W32 (DCF, out_bits <= 32): the sigma/tau block through mmo_sigma_tau32.
+template <bool CMP, bool W32 = false>
 __global__ void __launch_bounds__(kPairKeygenThreads, 1)
 keygen_pair_kernel(int n, int out_bits, uint64_t count, const uint64_t* __restrict__ alpha,
                    const uint64_t* __restrict__ alpha0, const uint8_t* __restrict__ s0_init,
@@ -630,7 +631,7 @@ keygen_pair_kernel(int n, int out_bits, uint64_t count, const uint64_t* __restri
             cws.w = side.w ^ __shfl_sync(pm, side.w, q);
             uint32_t g_x = 0, g_y = 0, g_z = 0, g_w = 0, h_x = 0, h_y = 0, h_z = 0, h_w = 0;
             if (CMP) {
-                const U4 g = fssb::mmo<2, false>(tb, s, 0);
+                const U4 g = W32 ? fssb::mmo_sigma_tau32<2>(tb, s) : fssb::mmo<2, false>(tb, s, 0);
                 g_x = g.x; g_y = g.y; g_z = g.z; g_w = g.w;
                 h_x = __shfl_sync(pm, g.x, q);
                 h_y = __shfl_sync(pm, g.y, q);
@@ -1286,14 +1287,13 @@ int fss_dcf_keygen(int n, int out_bits, uint64_t count, const uint64_t* alpha,
     FSS_REQUIRE(alpha, alpha0, s0, s1, scw, tcw, sigma_cw, leaf_cw, alpha1);
     int sms;
     if (FSSB_KEYGEN_PAIR_DCF) {
-        if (int rc = prep_launch(keygen_pair_kernel<true>, &sms)) return rc;
-        {
-            int threads;
-            const int grid = balanced_grid(2 * count, sms, kPairKeygenThreads, &threads);
-            keygen_pair_kernel<true><<<grid, threads, fssb::kTableBytes, (cudaStream_t)stream>>>(
-                n, out_bits, count, alpha, alpha0, s0, s1, scw, tcw, sigma_cw, leaf_cw, nullptr, alpha1);
-            return check_launch();
-        }
+        auto kern = FSSB_W32 && out_bits <= 32 ? keygen_pair_kernel<true, true> : keygen_pair_kernel<true, false>;
+        if (int rc = prep_launch(kern, &sms)) return rc;
+        int threads;
+        const int grid = balanced_grid(2 * count, sms, kPairKeygenThreads, &threads);
+        kern<<<grid, threads, fssb::kTableBytes, (cudaStream_t)stream>>>(
+            n, out_bits, count, alpha, alpha0, s0, s1, scw, tcw, sigma_cw, leaf_cw, nullptr, alpha1);
+        return check_launch();
     }
     if (int rc = prep_launch(dcf_keygen_kernel, &sms)) return rc;
     int threads;
