@@ -138,11 +138,12 @@ __device__ __forceinline__ uint32_t T(const Tab& tb, uint32_t c) {
     const uint32_t lo = (J & 1) ? tb.lo1 : tb.lo0;
     uint32_t addr;
 #if FSSB_IMAD_ADDR
-    if (K == 0) {         // addr = ((c << 24) * 2^16) >> 32 + lo = byte0 << 8 | lo
+    // FSSB_IMAD_ADDR: 1 = bytes 0 and 3 on the FMA pipe, 2 = byte 0 only, 3 = byte 3 only
+    if (K == 0 && FSSB_IMAD_ADDR != 3) {   // addr = ((c << 24) * 2^16) >> 32 + lo = byte0 << 8 | lo
         uint32_t t;
         asm("mul.lo.u32 %0, %1, %2;" : "=r"(t) : "r"(c), "r"(kAddrMul[0]));
         asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(t), "r"(kAddrMul[1]), "r"(lo));
-    } else if (K == 3) {  // addr = (c * 2^8) >> 32 = byte3, then * 2^8 + lo
+    } else if (K == 3 && FSSB_IMAD_ADDR != 2) {  // addr = (c * 2^8) >> 32 = byte3, then * 2^8 + lo
         uint32_t t;
         asm("mul.hi.u32 %0, %1, %2;" : "=r"(t) : "r"(c), "r"(kAddrMul[2]));
         asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(t), "r"(kAddrMul[2]), "r"(lo));
