@@ -1071,6 +1071,23 @@ void par_memcpy(void* dst, const void* src, size_t bytes) {
     }
 }
 
+// Size of staged chunk i starting at element lo. Long ranges ramp up and down
+// (chunk/4, chunk/2, chunk, ..., chunk, chunk/2, chunk/4): the first kernel
+// waits only for a quarter chunk's host copy + H2D, and after the last kernel
+// only a quarter chunk's D2H + host copy remains.
+#ifndef FSSB_STAGED_RAMP
+#define FSSB_STAGED_RAMP 1
+#endif
+uint64_t staged_chunk(uint64_t i, uint64_t lo, uint64_t count, uint64_t chunk) {
+    const uint64_t r = count - lo, q = chunk / 4;
+    if (!FSSB_STAGED_RAMP || count < 8 * chunk || q == 0) return r < chunk ? r : chunk;
+    uint64_t m = i == 0 ? q : (i == 1 ? 2 * q : chunk);
+    if (r <= q) return r;
+    if (r <= 3 * q) m = r - q < m ? r - q : m;                  // then the last quarter
+    else if (r <= chunk + 3 * q) m = r - 3 * q < m ? r - 3 * q : m;   // then a half, a quarter
+    return m < r ? m : r;
+}
+
 // Pageable host buffers (e.g. numpy arrays): chunks are staged through pinned
 // slots by host memcpy, which overlaps the other slot's copies and kernel.
 // Returns when every share is in out_host.
@@ -1092,8 +1109,8 @@ int run_host_pipe_staged(const HostPipe& hp, uint64_t count, Launch launch) {
         par_memcpy(hp.out_host + out_lo[k], sout[k], out_m[k] * 8);
         out_busy[k] = false;
     };
-    for (uint64_t i = 0, lo = 0; lo < count && rc == kOk; i++, lo += hp.chunk) {
-        const uint64_t m = count - lo < hp.chunk ? count - lo : hp.chunk;
+    for (uint64_t i = 0, lo = 0, m = 0; lo < count && rc == kOk; i++, lo += m) {
+        m = staged_chunk(i, lo, count, hp.chunk);
         const int slot = (int)(i & 1);
         cudaStream_t s = hp.st[slot];
         uint64_t* xd = hp.x_dev + slot * hp.chunk;
