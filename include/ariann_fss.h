@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define FSS_ABI_VERSION 5
+#define FSS_ABI_VERSION 6
 #define FSS_OK 0
 #define FSS_EINVAL 1
 #define FSS_ECUDA 2
@@ -135,12 +135,13 @@ int fss_dcf_eval_masked(int party, int n, int out_bits, uint64_t count, uint64_t
  * of the drop-in): [0, count) is streamed in `chunk`-element pieces over two
  * streams -- cudaMemcpyAsync of x_host (pinned) into x_dev, the eval kernel,
  * cudaMemcpyAsync of the shares into out_host (pinned) -- so copies overlap
- * kernels. x_dev / out_dev are caller scratch of 2 * chunk words each.
- * stage == NULL: x_host / out_host are pinned; returns once enqueued and the
- * caller synchronises stream_a and stream_b. stage != NULL (4 * chunk pinned
- * words): x_host / out_host may be pageable (numpy arrays); chunks are staged
- * by host memcpy overlapping the GPU work, and the call returns when out_host
- * is complete. */
+ * kernels. stage == NULL: x_host / out_host are pinned; x_dev / out_dev are
+ * caller scratch of 2 * chunk words each; returns once enqueued and the
+ * caller synchronises stream_a and stream_b. stage != NULL (6 * chunk pinned
+ * words; x_dev / out_dev then 3 * chunk words each): x_host / out_host may be
+ * pageable (numpy arrays); chunks are staged through three slots by host
+ * memcpy overlapping the GPU work, and the call returns when out_host is
+ * complete (ABI 6: three staging slots, ABI 5 had two). */
 int fss_dcf_eval_host(int party, int n, int out_bits, uint64_t count, uint64_t ld,
                       const uint8_t* seed0, const uint8_t* scw, const uint8_t* tcw,
                       const uint64_t* sigma_cw, const uint64_t* leaf_cw, const uint64_t* x_host,

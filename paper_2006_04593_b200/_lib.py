@@ -33,7 +33,7 @@ class Peaks(ctypes.Structure):
 
 
 # name -> argtypes (all return int status unless listed in _RESTYPE)
-ABI_VERSION = 5   # include/ariann_fss.h FSS_ABI_VERSION
+ABI_VERSION = 6   # include/ariann_fss.h FSS_ABI_VERSION
 
 SIGNATURES = {
     "fss_abi_version": [],

@@ -1091,17 +1091,34 @@ uint64_t staged_chunk(uint64_t i, uint64_t lo, uint64_t count, uint64_t chunk) {
 // Pageable host buffers (e.g. numpy arrays): chunks are staged through pinned
 // slots by host memcpy, which overlaps the other slot's copies and kernel.
 // Returns when every share is in out_host.
+// Three staging slots, drained two chunks behind: after enqueueing chunk i the
+// host copies out chunk i-2's shares, so a slow host copy (first-touch page
+// faults of a fresh numpy result) is absorbed while chunks i-1 and i are still
+// queued; with two slots the host waited on chunk i-1 and the GPU idled
+// whenever that copy outran one kernel (0.3-0.4 ms gaps in the trace).
+// Chunk i runs on stream i & 1 and uses slot i % 3; a slot is refilled only
+// after the drain of its previous chunk returned (kernel and D2H complete).
+#ifndef FSSB_STAGE_SLOTS
+#define FSSB_STAGE_SLOTS 3   // 2..3 (the buffers are sized for 3); drain lag = slots - 1
+#endif
+constexpr int kStageSlots = FSSB_STAGE_SLOTS;
+
 template <typename Launch>
 int run_host_pipe_staged(const HostPipe& hp, uint64_t count, Launch launch) {
-    cudaEvent_t h2d[2], d2h[2];
-    for (int k = 0; k < 2; k++) {
+    constexpr int K = kStageSlots;
+    cudaEvent_t h2d[K], d2h[K];
+    uint64_t* sin[K];
+    uint64_t* sout[K];
+    bool in_busy[K], out_busy[K];
+    uint64_t out_lo[K], out_m[K];
+    for (int k = 0; k < K; k++) {
         cudaEventCreateWithFlags(&h2d[k], cudaEventDisableTiming);
         cudaEventCreateWithFlags(&d2h[k], cudaEventDisableTiming);
+        sin[k] = hp.stage + k * hp.chunk;
+        sout[k] = hp.stage + (K + k) * hp.chunk;
+        in_busy[k] = out_busy[k] = false;
+        out_lo[k] = out_m[k] = 0;
     }
-    uint64_t* sin[2] = {hp.stage, hp.stage + hp.chunk};
-    uint64_t* sout[2] = {hp.stage + 2 * hp.chunk, hp.stage + 3 * hp.chunk};
-    bool in_busy[2] = {false, false}, out_busy[2] = {false, false};
-    uint64_t out_lo[2] = {0, 0}, out_m[2] = {0, 0};
     int rc = kOk;
     auto drain = [&](int k) {
         if (!out_busy[k]) return;
@@ -1109,12 +1126,14 @@ int run_host_pipe_staged(const HostPipe& hp, uint64_t count, Launch launch) {
         par_memcpy(hp.out_host + out_lo[k], sout[k], out_m[k] * 8);
         out_busy[k] = false;
     };
-    for (uint64_t i = 0, lo = 0, m = 0; lo < count && rc == kOk; i++, lo += m) {
+    uint64_t i = 0;
+    for (uint64_t lo = 0, m = 0; lo < count && rc == kOk; i++, lo += m) {
         m = staged_chunk(i, lo, count, hp.chunk);
-        const int slot = (int)(i & 1);
-        cudaStream_t s = hp.st[slot];
+        const int slot = (int)(i % K);
+        cudaStream_t s = hp.st[i & 1];
         uint64_t* xd = hp.x_dev + slot * hp.chunk;
         uint64_t* od = hp.out_dev + slot * hp.chunk;
+        drain(slot);                                          // chunk i-3 (normally done already)
         if (in_busy[slot]) cudaEventSynchronize(h2d[slot]);   // staging slot free again
         par_memcpy(sin[slot], hp.x_host + lo, m * 8);
         cudaError_t err = cudaMemcpyAsync(xd, sin[slot], m * 8, cudaMemcpyHostToDevice, s);
@@ -1125,20 +1144,18 @@ int run_host_pipe_staged(const HostPipe& hp, uint64_t count, Launch launch) {
         err = cudaMemcpyAsync(sout[slot], od, m * 8, cudaMemcpyDeviceToHost, s);
         if (err != cudaSuccess) { rc = set_err(kEcuda, "D2H: %s", cudaGetErrorString(err)); break; }
         cudaEventRecord(d2h[slot], s);
-        drain(slot ^ 1);                                      // previous chunk's shares
         out_busy[slot] = true;
         out_lo[slot] = lo;
         out_m[slot] = m;
+        if (i >= K - 1) drain((int)((i - (K - 1)) % K));      // K - 1 chunks behind
     }
     if (rc == kOk) {
-        const int first = out_busy[0] && out_busy[1] ? (out_lo[0] < out_lo[1] ? 0 : 1) : (out_busy[0] ? 0 : 1);
-        drain(first);
-        drain(first ^ 1);
+        for (uint64_t j = i >= K - 1 ? i - (K - 1) : 0; j < i; j++) drain((int)(j % K));   // in element order
     } else {
         cudaStreamSynchronize(hp.st[0]);
         cudaStreamSynchronize(hp.st[1]);
     }
-    for (int k = 0; k < 2; k++) {
+    for (int k = 0; k < K; k++) {
         cudaEventDestroy(h2d[k]);
         cudaEventDestroy(d2h[k]);
     }

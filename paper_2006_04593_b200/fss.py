@@ -879,12 +879,12 @@ def _run_eval(launch, xt, host, count: int, dev, host_launch=None, out=None):
     cur = torch.cuda.current_stream(dev)
     # device scratch on the current stream; the side streams wait for it and the
     # current stream waits for them, so the allocator cannot recycle it early
-    scratch = torch.empty((2, 2 * chunk), dtype=torch.uint64, device=dev)
+    scratch = torch.empty((2, 3 * chunk), dtype=torch.uint64, device=dev)   # 3 staging slots
     streams = _dev.side_streams(dev, 2)
     for st in streams:
         st.wait_stream(cur)
     out_host = np.empty(count, dtype=np.uint64)
-    stage = torch.empty(4 * chunk, dtype=torch.uint64, pin_memory=True)
+    stage = torch.empty(6 * chunk, dtype=torch.uint64, pin_memory=True)
     host_launch(xt.ctypes.data, out_host.ctypes.data, scratch[0], scratch[1], chunk,
                 stage.data_ptr(), streams[0].cuda_stream, streams[1].cuda_stream)
     for st in streams:

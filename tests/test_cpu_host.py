@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for sym in declared:
         assert hasattr(lib, sym), sym
     assert set(_lib.SIGNATURES) >= declared
-    assert lib.fss_abi_version() == 5
+    assert lib.fss_abi_version() == 6
     assert not hasattr(lib, "fss_aes_mmo_expand_bitsliced")   # research record, not product ABI
     assert lib.fss_arnk_elem_bytes(1, 32) == 824 and lib.fss_arnk_elem_bytes(0, 32) == 568
     assert isinstance(ctypes.CDLL(_build.LIB), ctypes.CDLL)
