@@ -736,16 +736,24 @@ arnk_pack_tma_kernel(const __grid_constant__ PackMaps M, int n, uint64_t count, 
 #ifndef FSSB_ARNK_TILE_KB
 #define FSSB_ARNK_TILE_KB 100
 #endif
+// Unpack: 128-key tiles (two buffers of 103 KB for DCF at n = 32, one CTA
+// of 512 threads per SM) write longer level-row segments per tile than 64-key
+// tiles at two CTAs per SM: DCF 0.873 -> 0.897, DPF 0.884 -> 0.920 of HBM
+// (scripts/arnk_bench.py variants un_t128*, profiles/r02_arnk_unpack_tiles.json);
+// 32-key tiles were worse, the thread count (128-1024) hardly matters.
 #ifndef FSSB_ARNK_UNPACK_TILE_KB
-#define FSSB_ARNK_UNPACK_TILE_KB 110
+#define FSSB_ARNK_UNPACK_TILE_KB 215
 #endif
 int arnk_tile_lnb(bool pack, int kind, int n) {
+    // the largest tile (16 << lnb keys, lnb <= 3) whose two buffers fit the budget
     const uint64_t kb = pack ? FSSB_ARNK_TILE_KB : FSSB_ARNK_UNPACK_TILE_KB;
-    return 2 * elem_bytes(kind, n) * 64 <= kb * 1024 ? 2 : 1;
+    int lnb = 1;
+    while (lnb < 3 && 2 * elem_bytes(kind, n) * (16u << (lnb + 1)) <= kb * 1024) lnb++;
+    return lnb;
 }
 
 #ifndef FSSB_ARNK_UNPACK_THREADS
-#define FSSB_ARNK_UNPACK_THREADS 256
+#define FSSB_ARNK_UNPACK_THREADS 512
 #endif
 #ifndef FSSB_ARNK_ASYNC_PACK
 #define FSSB_ARNK_ASYNC_PACK 1

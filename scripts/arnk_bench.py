@@ -32,6 +32,14 @@ VARIANTS = {
     "eq_s3": ["FSSB_ARNK_TMA_STAGES_EQ=3"],
     "tma256": ["FSSB_ARNK_TMA_THREADS=256"],
     "promo0": ["FSSB_ARNK_TMA_L2PROMO=0"],
+    # r02 unpack study: CTA size and tile size of the unpack tile kernel
+    "un512": ["FSSB_ARNK_UNPACK_THREADS=512"],
+    "un_t32": ["FSSB_ARNK_UNPACK_TILE_KB=60"],
+    "un512_t32": ["FSSB_ARNK_UNPACK_THREADS=512", "FSSB_ARNK_UNPACK_TILE_KB=60"],
+    "un128": ["FSSB_ARNK_UNPACK_THREADS=128"],
+    "un_t128": ["FSSB_ARNK_UNPACK_TILE_KB=215"],
+    "un_t128_512": ["FSSB_ARNK_UNPACK_TILE_KB=215", "FSSB_ARNK_UNPACK_THREADS=512"],
+    "un_t128_1024": ["FSSB_ARNK_UNPACK_TILE_KB=215", "FSSB_ARNK_UNPACK_THREADS=1024"],
 }
 if os.environ.get("ARNK_VARIANTS"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["ARNK_VARIANTS"].split(",")}
