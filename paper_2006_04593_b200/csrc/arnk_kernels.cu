@@ -728,9 +728,8 @@ arnk_pack_tma_kernel(const __grid_constant__ PackMaps M, int n, uint64_t count, 
     if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-// Tile of E = 16 << lnb elements, two tile buffers per CTA. Unpack: 64
-// elements whenever the two buffers fit 110 KiB (cmp n = 32: 2 x 52.7 KB, two
-// CTAs per SM); pack: 64 only up to 100 KiB, i.e. 32 for cmp n = 32 (four
+// Tile of E = 16 << lnb elements, two tile buffers per CTA. Pack (the
+// fallback tile kernel): 64 only up to 100 KiB, i.e. 32 for cmp n = 32 (four
 // CTAs per SM hide its row-load latency better) -- measured,
 // profiles/r01_arnk_variants.json. Largest record: cmp n = 63, 2,111 B.
 #ifndef FSSB_ARNK_TILE_KB
@@ -827,8 +826,19 @@ bool encode_map(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint
 #ifndef FSSB_ARNK_TMA_PACK
 #define FSSB_ARNK_TMA_PACK 1
 #endif
-#ifndef FSSB_ARNK_TMA_LNB
-#define FSSB_ARNK_TMA_LNB 0
+// Keys per TMA pack tile = 16 << lnb, per kind (scripts/arnk_bench.py, r02):
+// cmp 32-key tiles move the tile's rows in half as many TMA boxes per key and
+// pack at 1.20 vs 1.35 ms per 2^22 keys (6.67 TB/s, above the 1:1 copy peak:
+// the mix is read-heavy); eq stays at 16 (0.79 vs 0.84 ms).
+#ifdef FSSB_ARNK_TMA_LNB
+#define FSSB_ARNK_TMA_LNB_CMP FSSB_ARNK_TMA_LNB
+#define FSSB_ARNK_TMA_LNB_EQ FSSB_ARNK_TMA_LNB
+#endif
+#ifndef FSSB_ARNK_TMA_LNB_CMP
+#define FSSB_ARNK_TMA_LNB_CMP 1
+#endif
+#ifndef FSSB_ARNK_TMA_LNB_EQ
+#define FSSB_ARNK_TMA_LNB_EQ 0
 #endif
 
 // The TMA-staged pack when the layout allows it (returns false otherwise and
@@ -846,7 +856,7 @@ bool try_pack_tma(int n, uint64_t count, uint64_t ld, const Keys& k, uint8_t* bu
                             (uintptr_t)(KIND == 1 ? ((uintptr_t)k.sigma_cw | (uintptr_t)k.leaf_cw)
                                                   : (uintptr_t)k.cw_final);
     if (bases & 15) return false;
-    const int lnb = FSSB_ARNK_TMA_LNB;
+    const int lnb = KIND == 1 ? FSSB_ARNK_TMA_LNB_CMP : FSSB_ARNK_TMA_LNB_EQ;
     const uint32_t E = 16u << lnb;
     PackMaps M;
     memset(&M, 0, sizeof(M));

@@ -40,6 +40,14 @@ VARIANTS = {
     "un_t128": ["FSSB_ARNK_UNPACK_TILE_KB=215"],
     "un_t128_512": ["FSSB_ARNK_UNPACK_TILE_KB=215", "FSSB_ARNK_UNPACK_THREADS=512"],
     "un_t128_1024": ["FSSB_ARNK_UNPACK_TILE_KB=215", "FSSB_ARNK_UNPACK_THREADS=1024"],
+    # TMA pack with 32-key tiles (2 or 3 staging buffers)
+    "tma32": ["FSSB_ARNK_TMA_LNB=1"],
+    "tma32_s2": ["FSSB_ARNK_TMA_LNB=1", "FSSB_ARNK_TMA_STAGES_CMP=2"],
+    "tma32_1024": ["FSSB_ARNK_TMA_LNB=1", "FSSB_ARNK_TMA_THREADS=1024"],
+    "cmp32_s4": ["FSSB_ARNK_TMA_STAGES_CMP=4"],
+    "cmp32_256": ["FSSB_ARNK_TMA_THREADS=256"],
+    "eq32_s3": ["FSSB_ARNK_TMA_LNB_EQ=1", "FSSB_ARNK_TMA_STAGES_EQ=3"],
+    "eq32_1024": ["FSSB_ARNK_TMA_LNB_EQ=1", "FSSB_ARNK_TMA_THREADS=1024"],
 }
 if os.environ.get("ARNK_VARIANTS"):
     VARIANTS = {k: v for k, v in VARIANTS.items() if k in os.environ["ARNK_VARIANTS"].split(",")}
