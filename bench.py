@@ -356,6 +356,11 @@ def measure_secondary(dev, args):
     out["arnk_unpack_keys_per_s"] = N / t
     out["arnk_unpack_gb_per_s"] = N * per_key / t / 1e9
     out["arnk_algorithmic_bytes_per_key"] = per_key
+    out["arnk_note"] = ("arnk_*_frac_hbm is against MEASURED_PEAKS' 1:1 copy. Pack reads 1,088 B and writes "
+                        "824 B per key, a read-heavy mix that streams faster than a copy (read-only 7.36, "
+                        "write-only 6.36 TB/s on this part, scripts/hbm_mix_probe.cu), so pack can exceed 1; "
+                        "the time-additive roof of its mix is 6.89 TB/s, of unpack's (824 : 1,088) 6.76 TB/s "
+                        "(profiles/r02_arnk_tma_pack_tiles.json)")
     back = fss._unpack(fss.KIND_CMP, 0, N_BITS, N, payload, dev)
     assert torch.equal(back.scw, c0.scw) and torch.equal(back.leaf_cw.view(torch.int64),
                                                          c0.leaf_cw.view(torch.int64)), "ARNK round trip"
