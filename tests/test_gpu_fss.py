@@ -314,6 +314,28 @@ def test_host_paths_match_device_path():
     assert torch.equal(out_h, fss.eval_cmp(0, k0, xd).view(torch.int64).cpu())
 
 
+@pytest.mark.parametrize("chunks", [2.5, 7.9, 8.0, 9.3, 21.7])
+def test_staged_pipeline_schedule(monkeypatch, chunks):
+    # numpy x through the staged pipeline with a small chunk, so the three
+    # staging slots wrap several times and, from 8 chunks on, the quarter /
+    # half ramps at both ends are active; ragged tails included
+    chunk = 1 << 14
+    monkeypatch.setattr(fss, "PIPELINE_CHUNK", chunk)
+    monkeypatch.setattr(fss, "PIPELINE_MIN", chunk)
+    N = int(chunks * chunk) + 5
+    rng = np.random.default_rng(int(chunks * 10))
+    alpha, k0, k1 = fss.keygen_cmp(32, rng, N)
+    _, e0, _ = fss.keygen_eq(32, rng, N)
+    xn = np.random.default_rng(7).integers(0, 1 << 32, N, dtype=np.uint64)
+    xd = torch.from_numpy(xn.view(np.int64)).cuda().view(torch.uint64)
+    for party, k in ((0, k0), (1, k1)):
+        got = fss.eval_cmp(party, k, xn)
+        assert isinstance(got, np.ndarray) and got.shape == (N,)
+        assert np.array_equal(got, _np(fss.eval_cmp(party, k, xd).view(torch.int64)).view(np.uint64))
+    got = fss.eval_eq(0, e0, xn)
+    assert np.array_equal(got, _np(fss.eval_eq(0, e0, xd).view(torch.int64)).view(np.uint64))
+
+
 def test_bitsliced_expand_matches_ttable():
     # the bitsliced AES alternative (research record, scripts/research/bitsliced,
     # not in the product library) is bit-exact with the T-table PRG and the
