@@ -200,7 +200,9 @@ def _np_payload(k, kind, n):
 
 @pytest.mark.parametrize("kind,n,count", [("cmp", 32, 1024), ("cmp", 32, 4096), ("eq", 32, 2048),
                                           ("cmp", 12, 512), ("eq", 7, 320), ("cmp", 63, 64),
-                                          ("eq", 64, 96), ("cmp", 4, 48)])
+                                          ("eq", 64, 96), ("cmp", 4, 48),
+                                          # several tiles per CTA (persistent grid)
+                                          ("cmp", 32, 40000), ("eq", 32, 40000)])
 def test_pack_tensor_map_path_matches_numpy(kind, n, count):
     """Level strides that are multiples of 16 and even counts take the TMA
     tensor-map pack (arnk_pack_tma_kernel): whole batches, prefixes with a
@@ -220,7 +222,9 @@ def test_pack_tensor_map_path_matches_numpy(kind, n, count):
 
 
 @pytest.mark.parametrize("kind,n,count", [("cmp", 32, 1024), ("eq", 32, 2048), ("cmp", 12, 512),
-                                          ("eq", 7, 320), ("cmp", 63, 64), ("eq", 64, 96)])
+                                          ("eq", 7, 320), ("cmp", 63, 64), ("eq", 64, 96),
+                                          # several 128-key tiles per CTA (persistent grid)
+                                          ("cmp", 32, 40000), ("eq", 32, 40000)])
 def test_unpack_into_column_range(kind, n, count):
     """Unpack into fresh arrays and into a column range of padded arrays
     (ld > count, 16-aligned and unaligned column offsets, ragged last tiles):
