@@ -141,7 +141,8 @@ int fss_dcf_eval_masked(int party, int n, int out_bits, uint64_t count, uint64_t
  * words; x_dev / out_dev then 3 * chunk words each): x_host / out_host may be
  * pageable (numpy arrays); chunks are staged through three slots by host
  * memcpy overlapping the GPU work, and the call returns when out_host is
- * complete (ABI 6: three staging slots, ABI 5 had two). */
+ * complete (ABI 6: three staging slots, ABI 5 had two). A page-locked
+ * out_host receives the shares by D2H directly (no copy-out). */
 int fss_dcf_eval_host(int party, int n, int out_bits, uint64_t count, uint64_t ld,
                       const uint8_t* seed0, const uint8_t* scw, const uint8_t* tcw,
                       const uint64_t* sigma_cw, const uint64_t* leaf_cw, const uint64_t* x_host,

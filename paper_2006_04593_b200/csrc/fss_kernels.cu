@@ -1119,11 +1119,20 @@ int run_host_pipe_staged(const HostPipe& hp, uint64_t count, Launch launch) {
         in_busy[k] = out_busy[k] = false;
         out_lo[k] = out_m[k] = 0;
     }
+    // A page-locked out_host (the drop-in hands out pinned numpy results) takes
+    // the shares straight from the D2H copies: no staging slot, no copy-out.
+#ifndef FSSB_DIRECT_D2H
+#define FSSB_DIRECT_D2H 1
+#endif
+    cudaPointerAttributes pa;
+    const bool out_pinned = FSSB_DIRECT_D2H && cudaPointerGetAttributes(&pa, hp.out_host) == cudaSuccess &&
+                            pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();   // a pageable pointer may leave an error code behind
     int rc = kOk;
     auto drain = [&](int k) {
         if (!out_busy[k]) return;
         cudaEventSynchronize(d2h[k]);
-        par_memcpy(hp.out_host + out_lo[k], sout[k], out_m[k] * 8);
+        if (!out_pinned) par_memcpy(hp.out_host + out_lo[k], sout[k], out_m[k] * 8);
         out_busy[k] = false;
     };
     uint64_t i = 0;
@@ -1141,7 +1150,7 @@ int run_host_pipe_staged(const HostPipe& hp, uint64_t count, Launch launch) {
         cudaEventRecord(h2d[slot], s);
         in_busy[slot] = true;
         if ((rc = launch(lo, m, xd, od, s)) != kOk) break;
-        err = cudaMemcpyAsync(sout[slot], od, m * 8, cudaMemcpyDeviceToHost, s);
+        err = cudaMemcpyAsync(out_pinned ? hp.out_host + lo : sout[slot], od, m * 8, cudaMemcpyDeviceToHost, s);
         if (err != cudaSuccess) { rc = set_err(kEcuda, "D2H: %s", cudaGetErrorString(err)); break; }
         cudaEventRecord(d2h[slot], s);
         out_busy[slot] = true;
